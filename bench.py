@@ -1,0 +1,352 @@
+"""Benchmark: Gfragments/s of the fused wavelet OIT frame (build + evaluate + composite).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2|4]
+
+Workload (BASELINE.json configs[1], "config 2"): 1920x1080, 32 fragments/pixel
+synthetic smoke volume, rank 3 (16 Haar slots), fp32 CSR stream generated on the
+device (bit-identical to the numpy generator). One step = one full frame through
+the fused kernel: bounds, closed-form Haar build, per-fragment transmittance v̂
+(written, 12 B/fragment), visibility-weighted accumulation and composite (image
+written). Inputs (2.1 GB) are larger than L2 (126 MB), so no flush is needed.
+
+Multi-GPU (torchrun, one rank per GPU): weak scaling, rank r renders rows
+[1080 r, 1080 (r+1)) of a 1920 x 1080N frame and the fp32 image bands are
+all-gathered over NCCL inside the timed step; time = max over ranks.
+
+--impl reference times the reference's CPU algorithm (the numpy port in oracle/,
+a float64 restatement pinned against the reference's own outputs) on the host
+cores, on a bounded row band of the same workload per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "Gfragments/s (build+eval+composite) and % HBM roofline at 1/2/4/8 B200 vs CPU"
+UNIT = "Gfrag/s"
+CONFIGS = {
+    2: dict(workload="smoke", width=1920, height=1080, layers=32, rank=3, seed=1,
+            name="config2: 1080p synthetic smoke, 32 frag/px, rank 3 (16 coeffs), 1 B200"),
+    4: dict(workload="particles", width=3840, height=2160, layers=128, rank=3, seed=1,
+            name="config4: 4K particles, 128 frag/px, depth-varying alpha, rank 3"),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def algorithmic_bytes(npix: int, nfrag: int, rank: int) -> int:
+    """44 B/fragment (depth, alpha, T, L in; v̂ out) +
+    (32 + 12 S) B/pixel (offsets, opaque RGB in; coefficients, image out)."""
+    S = 1 << (rank + 1)
+    return nfrag * 44 + npix * (32 + 12 * S)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_reference(cfg, rows: int, steps: int, warmup: int):
+    """Time the reference algorithm (numpy port, all host threads) on `rows` rows."""
+    from oracle import woit_oracle as O
+    from paper_2201_00094_b200 import synth
+
+    workers = O.default_workers()
+    sf = synth.generate(cfg["workload"], cfg["width"], cfg["height"], seed=cfg["seed"], layers=cfg["layers"],
+                        row0=0, rows=rows)
+    frame = O.OFrame.from_synth(sf)
+    ocfg = O.OConfig(rank=cfg["rank"], width=cfg["width"], height=rows, workers=workers)
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        O.render_frame(frame, ocfg, workers=workers)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+    n = sf.nfrag
+    return n / float(np.mean(times)) / 1e9, workers, f"{rows} rows x {cfg['width']} px x {cfg['layers']} frag/px " \
+        f"= {n} fragments, float64 numpy port, {workers} threads", float(np.mean(times))
+
+
+def run_reference(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    rows = args.ref_rows
+    steps = max(1, min(args.steps, 3))
+    warm = 1 if args.warmup > 0 else 0
+    value, cores, sample, _ = cpu_reference(cfg, rows, steps, warm)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps, "warmup": warm,
+            "ms_per_step": rows * cfg["width"] * cfg["layers"] / (value * 1e9) * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": cfg["name"], "width": cfg["width"], "height": cfg["height"],
+                       "frag_per_px": cfg["layers"], "rank": cfg["rank"]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfg):
+    import torch
+
+    import paper_2201_00094_b200 as W
+    from paper_2201_00094_b200 import _lib
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    H1 = cfg["height"]
+    Wd = cfg["width"]
+    frame_h = H1 * world
+    # this rank's band of a weak-scaled frame: rows [H1*rank, H1*(rank+1))
+    frame = W.FrameFragments.synthetic(cfg["workload"], Wd, frame_h, seed=cfg["seed"], layers=cfg["layers"],
+                                       row0=H1 * rank, rows=H1, device=dev)
+    rcfg = W.RenderConfig(rank=cfg["rank"], width=Wd, height=frame_h)
+    lib = _lib.load()
+    P, n = frame.npix, frame.nfrag
+    S = 1 << (cfg["rank"] + 1)
+    coeffs = torch.empty(P, S, 3, dtype=torch.float32, device=dev)
+    vhat = torch.empty(n, 3, dtype=torch.float32, device=dev)
+    out = torch.empty(P, 3, dtype=torch.float32, device=dev)
+    image = torch.empty(P * world, 3, dtype=torch.float32, device=dev) if world > 1 else out
+    wsn = lib.woit_frame_workspace_bytes(P, n)
+    ws = torch.empty(wsn, dtype=torch.uint8, device=dev)
+    fs = frame.c_struct()
+    ps = W.pipeline._params(rcfg, cfg["rank"])
+    bs = _lib.Bufs()
+    bs.coeffs, bs.vhat, bs.output = coeffs.data_ptr(), vhat.data_ptr(), out.data_ptr()
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        _lib.check(lib.woit_render_band(fs, ps, bs, ws.data_ptr(), wsn, stream.cuda_stream), "render_band")
+        if world > 1:
+            pg.all_gather_into_tensor(image, out)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        pg.barrier()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)
+        torch.cuda.synchronize()
+        if world > 1:
+            pg.barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for i in range(args.steps):
+            starts[i].record(stream)
+            _lib.check(lib.woit_render_band(fs, ps, bs, ws.data_ptr(), wsn, stream.cuda_stream), "render_band")
+            kends[i].record(stream)
+            if world > 1:
+                pg.all_gather_into_tensor(image, out)
+            ends[i].record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            pg.barrier()
+    total_ms = t0.elapsed_time(t1)
+    kern_ms = float(np.mean([s.elapsed_time(k) for s, k in zip(starts, kends)]))
+    if world > 1:
+        t = torch.tensor([total_ms, kern_ms], device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        total_ms, kern_ms = float(t[0]), float(t[1])
+    ms = total_ms / args.steps
+    frags_total = n * world
+    value = frags_total / (ms * 1e-3) / 1e9
+
+    # end to end through the public API: pinned host stream -> device, render, image -> host
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, W, frame, rcfg, dev, world, pg)
+
+    peak, peak_kind = peaks()
+    alg = algorithmic_bytes(P, n, cfg["rank"])
+    achieved = alg / (kern_ms * 1e-3) / 1e9
+    clocks = clk.summary()
+    if rank != 0:
+        if pg is not None:
+            pg.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        v, cores, sample, secs = cpu_reference(cfg, args.ref_rows, 1, 0)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (z, indices and per-pixel sums in f64)", "data": "synthetic",
+        "config": {"workload": cfg["name"], "width": Wd, "height": frame_h, "frag_per_px": cfg["layers"],
+                   "rank": cfg["rank"], "fragments": frags_total, "l2_flush": "inputs 2.1 GB/GPU > 126 MB L2",
+                   "parallelism": f"row bands x{world}, NCCL image all-gather" if world > 1 else "1 GPU"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": args.traffic,
+                     "kernel": "frame_kernel<3> (fused bounds+build+eval+composite)",
+                     "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": alg, "peak_kind": peak_kind},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": 2 * args.steps,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.destroy_process_group()
+
+
+def run_e2e(args, W, frame, rcfg, dev, world, pg):
+    """Same metric through the public API with host buffers: every step copies the
+    step's fragment stream host->device (pinned), renders, and reads the image back."""
+    import torch
+
+    names = ("offsets", "depth", "alpha", "trans", "radiance", "opaque_color")
+    host = {k: torch.empty_like(getattr(frame, k), device="cpu").pin_memory() for k in names}
+    for k in names:
+        host[k].copy_(getattr(frame, k))
+    devbuf = {k: torch.empty_like(getattr(frame, k)) for k in names}
+    f2 = W.FrameFragments(frame.width, frame.height, devbuf["offsets"], devbuf["depth"], devbuf["alpha"],
+                          devbuf["trans"], devbuf["radiance"], frame.normal, frame.ior, frame.backface,
+                          frame.opaque_depth, devbuf["opaque_color"], frame.pixel_base, frame.frag_base)
+    bufs = W.FrameBuffers.allocate(f2, rcfg.rank)
+    img_host = torch.empty(frame.npix, 3, dtype=torch.float32).pin_memory()
+    h2d = sum(host[k].numel() * host[k].element_size() for k in names)
+    d2h = img_host.numel() * 4
+    ws = W.Workspace()
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        for k in names:
+            devbuf[k].copy_(host[k], non_blocking=True)
+        W.render_band(f2, rcfg, bufs=bufs, ws=ws)
+        img_host.copy_(bufs.output, non_blocking=True)
+
+    for _ in range(max(1, min(args.warmup, 2))):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        pg.barrier()
+    k = max(1, min(args.steps, 5))
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(k):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / k
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        ms = float(t[0])
+    return {"value": frame.nfrag * world / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": k}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", type=int, choices=sorted(CONFIGS), default=2)
+    ap.add_argument("--ref-rows", type=int, default=240, help="rows of the CPU sample")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="dram bytes per launch from an ncu --set full capture (profiles/)")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

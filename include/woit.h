@@ -1,0 +1,222 @@
+/*
+ * woit.h — C ABI of the B200-native wavelet OIT hot path (libwoit.so).
+ *
+ * The reference (`woit`, pure Python/numpy) has no FFI; its boundary for this
+ * path is a set of Python functions over numpy arrays. Each entry point below
+ * replaces one of them; the Python shim `paper_2201_00094_b200` binds them with
+ * ctypes exactly as INTEGRATION.md shows.
+ *
+ * Conventions
+ *  - every pointer argument is a DEVICE pointer unless stated otherwise;
+ *  - `stream` is a cudaStream_t (passed as void* so this header needs no CUDA
+ *    headers); 0 is the legacy default stream;
+ *  - the library never allocates or frees memory and keeps no global mutable
+ *    state: scratch is passed in as `ws`/`ws_bytes`, sized by the matching
+ *    *_workspace_bytes() query;
+ *  - calls are asynchronous and stream-ordered; the return value reports
+ *    argument validation and launch errors only (negative = error).
+ *  - results are deterministic: per-pixel reductions run in an order fixed by
+ *    the CSR order, the pixel id and the fragment id, so any row-band split
+ *    (pixel_base/frag_base) yields bit-identical outputs.
+ *
+ * Data layout (SoA, CSR by pixel — the reference's FrameFragments contract,
+ * scene.py:367-392, in fp32 instead of f64):
+ *   offsets  int64 [npix+1]          fragments of pixel p are [offsets[p], offsets[p+1])
+ *   depth, alpha, ior   float [n]
+ *   trans, radiance, normal float [n][3]
+ *   backface uint8 [n]
+ *   opaque_depth float [npix] (+inf = no opaque hit), opaque_color float [npix][3]
+ * Per-pixel buffers (FrameBuffers, pipeline.py:76-104):
+ *   near, far float [npix]; coeffs float [npix][S][3] with S = 2^(rank+1)
+ *   (slot 0 = scaling coefficient, slot 2^n+k = level n offset k,
+ *   wavelet.py:3-9); accum, weight, output float [npix][3];
+ *   refraction_offset float [npix][2]; vhat float [n][3].
+ */
+#ifndef WOIT_H
+#define WOIT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WOIT_ABI_VERSION 1
+
+/* status codes */
+#define WOIT_OK 0
+#define WOIT_EINVAL (-1)      /* bad argument (null pointer, size, rank, flags) */
+#define WOIT_EWORKSPACE (-2)  /* ws_bytes smaller than the *_workspace_bytes query */
+#define WOIT_ECUDA (-3)       /* a CUDA launch / API call failed */
+#define WOIT_ERANK (-4)       /* rank outside [0, 6] (pipeline.py:66-67) */
+#define WOIT_ETAPS (-5)       /* aberration taps even or < 3 (pipeline.py:68-69) */
+
+/* RenderConfig booleans (pipeline.py:45-61) */
+#define WOIT_REFRACTION 0x01
+#define WOIT_CHROMATIC_ABERRATION 0x02
+#define WOIT_CUBE_TRANSMISSION 0x04
+#define WOIT_NORMALIZE 0x08
+#define WOIT_PACKED_STORAGE 0x10
+#define WOIT_LITERAL_SPECTRAL_T 0x20
+#define WOIT_CUBE_BACKFACE_ONLY 0x40
+
+typedef struct woit_frags {
+    int32_t width;        /* full frame width  (RenderConfig.width)  */
+    int32_t height;       /* full frame height (RenderConfig.height) */
+    int64_t npix;         /* pixels in this band = len(offsets) - 1   */
+    int64_t nfrag;        /* element count of the fragment arrays (>= offsets[npix]) */
+    int64_t pixel_base;   /* global id of the band's first pixel (pipeline.py:321-330) */
+    int64_t frag_base;    /* global id of fragment index 0 of this band's arrays */
+    const int64_t* offsets;
+    const float* depth;
+    const float* alpha;
+    const float* trans;
+    const float* radiance;
+    const float* normal;        /* may be NULL unless WOIT_REFRACTION */
+    const float* ior;           /* may be NULL: all 1.0 */
+    const uint8_t* backface;    /* may be NULL: all false */
+    const float* opaque_depth;  /* may be NULL: all +inf */
+    const float* opaque_color;  /* band-local [npix][3] */
+} woit_frags_t;
+
+typedef struct woit_params {
+    int32_t rank;            /* N, 0..6 */
+    int32_t flags;           /* WOIT_* booleans */
+    int32_t aberration_taps; /* odd, >= 3 */
+    int32_t reserved;
+    double refraction_scale; /* pixels per world unit at width 512 */
+    double cam_forward[3];   /* Camera.basis() (scene.py:141-150) */
+    double cam_right[3];
+    double cam_up[3];
+    double tan_half;         /* tan(fov/2) (scene.py:201) */
+    double aspect;           /* width / height */
+} woit_params_t;
+
+typedef struct woit_bufs {
+    float* near;               /* NULL: not written */
+    float* far;
+    float* coeffs;
+    float* accum;
+    float* weight;
+    float* refraction_offset;
+    float* output;
+    float* vhat;               /* per-fragment transmittance; NULL: not written */
+    const float* full_opaque_image; /* [height][width][3] for refraction / aberration gathers;
+                                       NULL: the band's opaque_color with pixel_base 0 */
+} woit_bufs_t;
+
+/* ---- version / errors ---------------------------------------------------- */
+int woit_abi_version(void);
+const char* woit_status_string(int status);
+
+/* ---- frame path (pipeline.py) -------------------------------------------- */
+
+/* Scratch for the frame and step entry points. */
+size_t woit_frame_workspace_bytes(int64_t npix, int64_t nfrag);
+
+/* All four passes fused over one row band, fragments read from HBM once.
+ * Replaces pipeline._wavelet_band (pipeline.py:321-330) on freshly allocated
+ * FrameBuffers: every non-NULL buffer in `bufs` is overwritten. */
+int woit_render_band(const woit_frags_t* frags, const woit_params_t* params, woit_bufs_t* bufs,
+                     void* ws, size_t ws_bytes, void* stream);
+
+/* step1_depth_bounds (pipeline.py:131-134): near = min(near, depth), far = max(far, depth). */
+int woit_step1_depth_bounds(const woit_frags_t* frags, woit_bufs_t* bufs, void* ws,
+                            size_t ws_bytes, void* stream);
+
+/* step2_build (pipeline.py:148-155): coeffs += closed-form Haar projection of every
+ * fragment's absorbance step, using bufs->near/far; packed storage if flagged. */
+int woit_step2_build(const woit_frags_t* frags, const woit_params_t* params, woit_bufs_t* bufs,
+                     void* ws, size_t ws_bytes, void* stream);
+
+/* step3_accumulate (pipeline.py:170-217): accum/weight/refraction_offset += ... from
+ * bufs->coeffs, near, far; writes vhat if non-NULL. */
+int woit_step3_accumulate(const woit_frags_t* frags, const woit_params_t* params,
+                          woit_bufs_t* bufs, void* ws, size_t ws_bytes, void* stream);
+
+/* step4_composite (pipeline.py:284-308): output from coeffs, accum, weight,
+ * refraction_offset and the background. Only width/height/npix/pixel_base and
+ * opaque_color of `frags` are read. */
+int woit_step4_composite(const woit_frags_t* frags, const woit_params_t* params,
+                         woit_bufs_t* bufs, void* stream);
+
+/* Per-fragment normalised depth z (double[n]), level slot offsets k_n
+ * (int32[n][rank+1], wavelet.py:281) and interpolation cells c0, c1
+ * (int32[n][2], wavelet.py:309-315), computed by the same device functions the
+ * frame kernels use, from bufs near/far. For bit-exact index parity checks. */
+int woit_fragment_indices(const woit_frags_t* frags, const float* near, const float* far, int rank,
+                          double* z, int32_t* slots, int32_t* cells, void* stream);
+
+/* ---- batch kernels (wavelet.py:272-337) ------------------------------------
+ * Same dtypes as the reference (float64 throughout). With WOIT_BUILD_BINNED the
+ * per-slot additions happen in fragment order in f64 with no FMA contraction,
+ * i.e. in exactly the order np.add.at performs them, so results are
+ * bit-identical to the reference's. coeffs is double[npix][2^(rank+1)][3]. */
+
+#define WOIT_BUILD_BINNED 0   /* stable sort by pixel, per-pixel ordered f64 sums */
+#define WOIT_BUILD_ATOMIC 1   /* red.global.add.f64 straight into coeffs (unordered) */
+
+size_t woit_build_into_workspace_bytes(int64_t n, int64_t npix);
+
+/* build_into (wavelet.py:272-287): coeffs[pix[i]] += projection of (z[i], a[i]) for
+ * arbitrary (unbinned) pixel ids. z: double[n], a: double[n][3]. */
+int woit_build_into(double* coeffs, int64_t npix, const int64_t* pix, const double* z,
+                    const double* a, int64_t n, int rank, int mode, void* ws, size_t ws_bytes,
+                    void* stream);
+
+/* interp_absorbance_batch (wavelet.py:306-319) -> out double[n][3] */
+int woit_interp_absorbance(const double* coeffs, int64_t npix, const int64_t* pix,
+                           const double* z, int64_t n, int rank, double* out, void* stream);
+
+/* cells_raw_batch (wavelet.py:290-303) -> out double[n][3] */
+int woit_cells_raw(const double* coeffs, int64_t npix, const int64_t* pix, const int64_t* cells,
+                   int64_t n, int rank, double* out, void* stream);
+
+/* total_absorbance_batch (wavelet.py:322-337) -> out double[npix][3] */
+int woit_total_absorbance(const double* coeffs, int64_t npix, int rank, double* out,
+                          void* stream);
+
+/* ---- fragment binning (scene.py:559-566 contract) ------------------------ */
+
+size_t woit_bin_workspace_bytes(int64_t n, int64_t npix);
+
+/* Stable counting sort of fragment ids by pixel: offsets[npix+1] equals
+ * concatenate([0], cumsum(bincount(pix, minlength=npix))) and perm lists the
+ * fragment ids of each pixel in their original order (np.argsort(pix, kind="stable")). */
+int woit_bin_by_pixel(const int64_t* pix, int64_t n, int64_t npix, int64_t* offsets,
+                      int64_t* perm, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- E5B9G9R9 packing (packing.py:46-111) --------------------------------- */
+
+/* words[i] = pack(|v[i][0..2]|) ; v is double[n][3] */
+int woit_pack_rgb9e5(const double* v, int64_t n, uint32_t* words, void* stream);
+/* out[i][0..2] = unpack(words[i]) */
+int woit_unpack_rgb9e5(const uint32_t* words, int64_t n, double* out, void* stream);
+
+/* ---- synthetic streams (paper_2201_00094_b200/synth.py twin) ------------- */
+
+#define WOIT_SYNTH_PLANE4 0
+#define WOIT_SYNTH_SMOKE 1
+#define WOIT_SYNTH_PARTICLES 2
+#define WOIT_SYNTH_RAGGED 3
+
+size_t woit_synth_workspace_bytes(int64_t npix);
+
+/* CSR offsets[rows*width+1] of band [row0, row0+rows): per-pixel run lengths and
+ * their scan (offsets[0] = 0). */
+int woit_synth_offsets(int workload, int32_t width, int32_t height, uint32_t seed, int32_t layers,
+                       int32_t row0, int32_t rows, int64_t* offsets, void* ws, size_t ws_bytes,
+                       void* stream);
+
+/* Fill the fragment arrays of the band from its offsets (all arrays non-NULL). */
+int woit_synth_fill(int workload, int32_t width, int32_t height, uint32_t seed, int32_t layers,
+                    int32_t row0, int32_t rows, const int64_t* offsets, float* depth,
+                    float* alpha, float* trans, float* radiance, float* normal, float* ior,
+                    uint8_t* backface, float* opaque_depth, float* opaque_color, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WOIT_H */

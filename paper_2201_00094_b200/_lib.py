@@ -1,0 +1,121 @@
+"""ctypes binding of libwoit.so (include/woit.h).
+
+The library is the only compute path: if it is missing or cannot be loaded the
+import fails loudly — there is no CPU or PyTorch fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libwoit.so")
+
+ABI_VERSION = 1
+
+OK = 0
+EINVAL = -1
+EWORKSPACE = -2
+ECUDA = -3
+ERANK = -4
+ETAPS = -5
+
+REFRACTION = 0x01
+CHROMATIC_ABERRATION = 0x02
+CUBE_TRANSMISSION = 0x04
+NORMALIZE = 0x08
+PACKED_STORAGE = 0x10
+LITERAL_SPECTRAL_T = 0x20
+CUBE_BACKFACE_ONLY = 0x40
+
+BUILD_BINNED = 0
+BUILD_ATOMIC = 1
+
+SYNTH_IDS = {"plane4": 0, "smoke": 1, "particles": 2, "ragged": 3}
+
+_vp = C.c_void_p
+_i32 = C.c_int32
+_i64 = C.c_int64
+_sz = C.c_size_t
+
+
+class Frags(C.Structure):
+    _fields_ = [("width", _i32), ("height", _i32), ("npix", _i64), ("nfrag", _i64),
+                ("pixel_base", _i64), ("frag_base", _i64), ("offsets", _vp), ("depth", _vp),
+                ("alpha", _vp), ("trans", _vp), ("radiance", _vp), ("normal", _vp), ("ior", _vp),
+                ("backface", _vp), ("opaque_depth", _vp), ("opaque_color", _vp)]
+
+
+class Params(C.Structure):
+    _fields_ = [("rank", _i32), ("flags", _i32), ("aberration_taps", _i32), ("reserved", _i32),
+                ("refraction_scale", C.c_double), ("cam_forward", C.c_double * 3),
+                ("cam_right", C.c_double * 3), ("cam_up", C.c_double * 3),
+                ("tan_half", C.c_double), ("aspect", C.c_double)]
+
+
+class Bufs(C.Structure):
+    _fields_ = [("near", _vp), ("far", _vp), ("coeffs", _vp), ("accum", _vp), ("weight", _vp),
+                ("refraction_offset", _vp), ("output", _vp), ("vhat", _vp),
+                ("full_opaque_image", _vp)]
+
+
+_SIGS = {
+    "woit_abi_version": (C.c_int, []),
+    "woit_status_string": (C.c_char_p, [C.c_int]),
+    "woit_frame_workspace_bytes": (_sz, [_i64, _i64]),
+    "woit_render_band": (C.c_int, [C.POINTER(Frags), C.POINTER(Params), C.POINTER(Bufs), _vp, _sz, _vp]),
+    "woit_step1_depth_bounds": (C.c_int, [C.POINTER(Frags), C.POINTER(Bufs), _vp, _sz, _vp]),
+    "woit_step2_build": (C.c_int, [C.POINTER(Frags), C.POINTER(Params), C.POINTER(Bufs), _vp, _sz, _vp]),
+    "woit_step3_accumulate": (C.c_int, [C.POINTER(Frags), C.POINTER(Params), C.POINTER(Bufs), _vp, _sz,
+                                        _vp]),
+    "woit_step4_composite": (C.c_int, [C.POINTER(Frags), C.POINTER(Params), C.POINTER(Bufs), _vp]),
+    "woit_fragment_indices": (C.c_int, [C.POINTER(Frags), _vp, _vp, C.c_int, _vp, _vp, _vp, _vp]),
+    "woit_build_into_workspace_bytes": (_sz, [_i64, _i64]),
+    "woit_build_into": (C.c_int, [_vp, _i64, _vp, _vp, _vp, _i64, C.c_int, C.c_int, _vp, _sz, _vp]),
+    "woit_interp_absorbance": (C.c_int, [_vp, _i64, _vp, _vp, _i64, C.c_int, _vp, _vp]),
+    "woit_cells_raw": (C.c_int, [_vp, _i64, _vp, _vp, _i64, C.c_int, _vp, _vp]),
+    "woit_total_absorbance": (C.c_int, [_vp, _i64, C.c_int, _vp, _vp]),
+    "woit_bin_workspace_bytes": (_sz, [_i64, _i64]),
+    "woit_bin_by_pixel": (C.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "woit_pack_rgb9e5": (C.c_int, [_vp, _i64, _vp, _vp]),
+    "woit_unpack_rgb9e5": (C.c_int, [_vp, _i64, _vp, _vp]),
+    "woit_synth_workspace_bytes": (_sz, [_i64]),
+    "woit_synth_offsets": (C.c_int, [C.c_int, _i32, _i32, C.c_uint32, _i32, _i32, _i32, _vp, _vp, _sz,
+                                     _vp]),
+    "woit_synth_fill": (C.c_int, [C.c_int, _i32, _i32, C.c_uint32, _i32, _i32, _i32, _vp, _vp, _vp, _vp,
+                                  _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib: Optional[C.CDLL] = None
+
+
+def load() -> C.CDLL:
+    """Load libwoit.so once; raise ImportError (no fallback) if it is unavailable."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2201_00094_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.woit_abi_version() != ABI_VERSION:
+        raise ImportError(f"libwoit ABI {lib.woit_abi_version()} != expected {ABI_VERSION}")
+    _lib = lib
+    return lib
+
+
+def check(status: int, what: str) -> None:
+    if status == OK:
+        return
+    msg = f"{what}: {load().woit_status_string(status).decode()} (status {status})"
+    if status in (EINVAL, ERANK, ETAPS, EWORKSPACE):
+        raise ValueError(msg)
+    raise RuntimeError(msg)

@@ -1,0 +1,240 @@
+// Frame-path kernels: the fused four-pass compositor (bounds -> build -> eval
+// -> composite) over CSR pixel tiles staged in shared memory by TMA bulk copies,
+// plus the long-pixel kernel and the standalone composite kernel.
+//
+// Reference: pipeline.py:131-308 (steps 1-4), wavelet.py:272-337 (batch math).
+// Design notes, smem layout and the roofline argument: DESIGN.md.
+#pragma once
+
+#include "common.cuh"
+#include "packing.cuh"
+
+namespace woit {
+
+// which passes a launch performs (the step entry points use subsets)
+enum : uint32_t {
+    PH_BOUNDS = 1u,       // near/far from the fragments (else read bufs->near/far)
+    PH_BOUNDS_ACC = 2u,   // ... combined with the existing bufs->near/far (step1)
+    PH_BUILD = 4u,        // coefficients from the fragments (else read bufs->coeffs)
+    PH_BUILD_ACC = 8u,    // ... added to the existing bufs->coeffs (step2)
+    PH_EVAL = 16u,        // v̂, accum, weight, refraction offset
+    PH_EVAL_ACC = 32u,    // ... added to the existing bufs accumulators (step3)
+    PH_COMPOSITE = 64u,   // output
+};
+
+struct KParams {
+    woit_frags_t f;
+    woit_params_t p;
+    woit_bufs_t b;
+    uint32_t phases;
+    int32_t use_tma;
+    int64_t* long_list;  // [0] = count, [1..] = band-local pixel ids
+    int64_t long_cap;
+};
+
+// per-rank tile geometry
+template <int R>
+struct RT {
+    static constexpr int S = 1 << (R + 1);   // coefficient slots (== cells M)
+    static constexpr int V = 3 * S;          // values per pixel
+    static constexpr int T = R <= 4 ? 128 : (R == 5 ? 64 : 32);  // threads = chunk slots
+    static constexpr int CH = 16;            // fragments per chunk (max)
+    static constexpr int FB = T * CH;        // fragments per sub-tile (max)
+    static constexpr int PB_RAW = 24576 / (V * 8);
+    static constexpr int PB = PB_RAW < T ? PB_RAW : T;  // pixels per CTA window
+    static constexpr int VP = V + 1;         // padded coef64 row
+};
+
+struct Layout {
+    uint32_t offs, nch, cb, nearu, faru, lo, den, vtot, chunk;
+    uint32_t depth, alpha, trans, rad, ior, normal, bf, zfix, r1, r2, bar, total;
+};
+
+WOIT_HD uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
+
+template <int R>
+WOIT_HD Layout make_layout(uint32_t phases, int flags) {
+    using G = RT<R>;
+    const bool frag = phases & (PH_BOUNDS | PH_BUILD | PH_EVAL);
+    const bool at = phases & (PH_BUILD | PH_EVAL);
+    const bool ev = phases & PH_EVAL;
+    const bool need_ior = at && (flags & (WOIT_CUBE_TRANSMISSION | WOIT_REFRACTION));
+    const bool need_bf = at && (flags & WOIT_CUBE_TRANSMISSION) && (flags & WOIT_CUBE_BACKFACE_ONLY);
+    const bool need_nrm = ev && (flags & WOIT_REFRACTION);
+    const uint32_t FS = G::FB + 4;  // staging window: [fa & ~3, fb)
+    Layout L;
+    uint32_t o = 0;
+    L.offs = o;  o = align16(o + 8u * (G::PB + 1));
+    L.nch = o;   o = align16(o + 8u * G::PB);
+    L.cb = o;    o = align16(o + 8u * (G::T + 1));
+    L.nearu = o; o = align16(o + 4u * G::PB);
+    L.faru = o;  o = align16(o + 4u * G::PB);
+    L.lo = o;    o = align16(o + 8u * G::PB);
+    L.den = o;   o = align16(o + 8u * G::PB);
+    L.vtot = o;  o = align16(o + 8u * 3 * G::PB);
+    L.chunk = o; o = align16(o + 4u * G::T);
+    L.depth = o; o = align16(o + (frag ? 4u * FS : 0u));
+    L.alpha = o; o = align16(o + (at ? 4u * FS : 0u));
+    L.trans = o; o = align16(o + (at ? 12u * FS : 0u));
+    L.rad = o;   o = align16(o + (ev ? 12u * FS : 0u));
+    L.ior = o;   o = align16(o + (need_ior ? 4u * FS : 0u));
+    L.normal = o; o = align16(o + (need_nrm ? 12u * FS : 0u));
+    L.bf = o;    o = align16(o + (need_bf ? (uint32_t)G::FB + 32u : 0u));
+    L.zfix = o;  o = align16(o + ((phases & PH_BUILD) && ev ? 8u * G::FB : 0u));
+    const uint32_t r1a = 4u * G::V * G::T, r1b = 4u * G::PB * G::V;
+    L.r1 = o;    o = align16(o + (r1a > r1b ? r1a : r1b));
+    const uint32_t r2a = 8u * G::PB * G::VP, r2b = 4u * 8u * G::T;
+    L.r2 = o;    o = align16(o + (r2a > r2b ? r2a : r2b));
+    L.bar = o;   o = align16(o + 16u);
+    L.total = o;
+    return L;
+}
+
+// ---------------------------------------------------------------------------
+// composite of one pixel (pipeline.py:242-308)
+
+WOIT_D double smoothstep_d(double e0, double e1, double x) {
+    double u = (x - e0) / (e1 - e0);
+    u = fmin(1.0, fmax(0.0, u));
+    return u * u * (3.0 - 2.0 * u);
+}
+
+// spectral_weight (pipeline.py:226-239)
+WOIT_D void spectral_weight(int i, int k, bool literal, double w[3]) {
+    const double t = literal ? 0.5 + 2.0 * i / (double)(k - 1) : i / (double)(k - 1);
+    const double wr = smoothstep_d(0.5, 1.0 / 3.0, t);
+    const double wb = smoothstep_d(0.5, 2.0 / 3.0, t);
+    w[0] = wr;
+    w[1] = 1.0 - wr - wb;
+    w[2] = wb;
+}
+
+// bilinear_sample (pipeline.py:242-255): edge clamped, in f64
+WOIT_D void bilinear(const float* __restrict__ img, int W, int H, double x, double y,
+                     double out[3]) {
+    x = fmin(fmax(x, 0.0), (double)W - 1.0);
+    y = fmin(fmax(y, 0.0), (double)H - 1.0);
+    const double fx = floor(x), fy = floor(y);
+    const int x0 = (int)fx, y0 = (int)fy;
+    const int x1 = min(x0 + 1, W - 1), y1 = min(y0 + 1, H - 1);
+    const double tx = x - fx, ty = y - fy;
+    const float* a = img + ((int64_t)y0 * W + x0) * 3;
+    const float* b = img + ((int64_t)y0 * W + x1) * 3;
+    const float* c = img + ((int64_t)y1 * W + x0) * 3;
+    const float* d = img + ((int64_t)y1 * W + x1) * 3;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        const double top = dadd(dmul((double)a[ch], 1.0 - tx), dmul((double)b[ch], tx));
+        const double bot = dadd(dmul((double)c[ch], 1.0 - tx), dmul((double)d[ch], tx));
+        out[ch] = dadd(dmul(top, 1.0 - ty), dmul(bot, ty));
+    }
+}
+
+// step4_composite for pixel p (band-local). accum/weight/refr are the pixel's
+// final accumulators, vtot = exp(-A_total).
+WOIT_D void composite_pixel(const KParams& kp, int64_t p, const double acc[3],
+                            const double wgt[3], double ox, double oy, const double vtot[3],
+                            float out[3]) {
+    const int W = kp.f.width;
+    const int flags = kp.p.flags;
+    double bg[3];
+    if (flags & (WOIT_CHROMATIC_ABERRATION | WOIT_REFRACTION)) {
+        const float* img = kp.b.full_opaque_image;
+        int H = kp.f.height;
+        int64_t gp = kp.f.pixel_base + p;
+        if (img == nullptr) {  // band-local image, as step4 without full_opaque_image
+            img = kp.f.opaque_color;
+            H = (int)(kp.f.npix / W);
+            gp = p;
+        }
+        const double px = (double)(gp % W), py = (double)(gp / W);
+        if (flags & WOIT_CHROMATIC_ABERRATION) {
+            const int k = kp.p.aberration_taps;
+            const bool lit = flags & WOIT_LITERAL_SPECTRAL_T;
+            double num[3] = {0.0, 0.0, 0.0}, den[3] = {0.0, 0.0, 0.0};
+            for (int i = 0; i < k; ++i) {
+                double w[3], s[3];
+                spectral_weight(i, k, lit, w);
+                const double fac = 2.0 * i / (double)(k - 1);
+                bilinear(img, W, H, dadd(px, dmul(ox, fac)), dadd(py, dmul(oy, fac)), s);
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) {
+                    num[ch] = dadd(num[ch], dmul(w[ch], s[ch]));
+                    den[ch] = dadd(den[ch], w[ch]);
+                }
+            }
+            double ctr[3];
+            bilinear(img, W, H, dadd(px, ox), dadd(py, oy), ctr);
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) bg[ch] = den[ch] > 0.0 ? ddiv(num[ch], den[ch]) : ctr[ch];
+        } else {
+            bilinear(img, W, H, dadd(px, ox), dadd(py, oy), bg);
+        }
+    } else {
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) bg[ch] = (double)kp.f.opaque_color[p * 3 + ch];
+    }
+    if (flags & WOIT_NORMALIZE) {
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            const double avg = ddiv(acc[ch], fmax(kNormEps, wgt[ch]));
+            out[ch] = (float)dadd(dmul(avg, 1.0 - vtot[ch]), dmul(bg[ch], vtot[ch]));
+        }
+    } else {
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) out[ch] = (float)dadd(acc[ch], dmul(bg[ch], vtot[ch]));
+    }
+}
+
+// Primary ray direction of global pixel gp (scene.py:199-212), f64.
+WOIT_D void ray_dir(const KParams& kp, int64_t gp, double d[3]) {
+    const int W = kp.f.width, H = kp.f.height;
+    const double px = (double)(gp % W), py = (double)(gp / W);
+    const double u = dmul(dmul(dsub(ddiv(dmul(2.0, dadd(px, 0.5)), (double)W), 1.0), kp.p.tan_half),
+                          kp.p.aspect);
+    const double v = dmul(dsub(1.0, ddiv(dmul(2.0, dadd(py, 0.5)), (double)H)), kp.p.tan_half);
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+        d[i] = dadd(dadd(kp.p.cam_forward[i], dmul(u, kp.p.cam_right[i])), dmul(v, kp.p.cam_up[i]));
+    const double nrm = sqrt(dadd(dadd(dmul(d[0], d[0]), dmul(d[1], d[1])), dmul(d[2], d[2])));
+#pragma unroll
+    for (int i = 0; i < 3; ++i) d[i] = ddiv(d[i], nrm);
+}
+
+// Screen-space refraction offset of one ior>1 fragment (pipeline.py:189-217).
+WOIT_D void refraction_offset(const KParams& kp, const double d[3], double t_opq, float depth,
+                              const float nrm[3], float ior, double off[2]) {
+    off[0] = 0.0;
+    off[1] = 0.0;
+    const double n0 = nrm[0], n1 = nrm[1], n2 = nrm[2];
+    const double ci = -dadd(dadd(dmul(d[0], n0), dmul(d[1], n1)), dmul(d[2], n2));
+    const double eta = ddiv(1.0, (double)ior);
+    const double s2 = dmul(dmul(eta, eta), dsub(1.0, dmul(ci, ci)));
+    bool ok = (ci > kDirEps) && (s2 <= 1.0) && isfinite(t_opq);
+    const double root = sqrt(fmax(dsub(1.0, s2), 0.0));
+    const double g = dsub(dmul(eta, ci), root);
+    const double td0 = dadd(dmul(eta, d[0]), dmul(g, n0));
+    const double td1 = dadd(dmul(eta, d[1]), dmul(g, n1));
+    const double td2 = dadd(dmul(eta, d[2]), dmul(g, n2));
+    const double* F = kp.p.cam_forward;
+    const double tdf = dadd(dadd(dmul(td0, F[0]), dmul(td1, F[1])), dmul(td2, F[2]));
+    const double dirf = dadd(dadd(dmul(d[0], F[0]), dmul(d[1], F[1])), dmul(d[2], F[2]));
+    ok = ok && (tdf > kDirEps);
+    if (!ok) return;
+    const double x = depth;
+    const double s = ddiv(dsub(dmul(t_opq, dirf), dmul(x, dirf)), tdf);
+    const double w0 = dsub(dadd(dmul(x, d[0]), dmul(s, td0)), dmul(t_opq, d[0]));
+    const double w1 = dsub(dadd(dmul(x, d[1]), dmul(s, td1)), dmul(t_opq, d[1]));
+    const double w2 = dsub(dadd(dmul(x, d[2]), dmul(s, td2)), dmul(t_opq, d[2]));
+    const double* Rv = kp.p.cam_right;
+    const double* U = kp.p.cam_up;
+    const double scale = dmul(kp.p.refraction_scale, ddiv((double)kp.f.width, 512.0));
+    const double ox = dmul(dadd(dadd(dmul(w0, Rv[0]), dmul(w1, Rv[1])), dmul(w2, Rv[2])), scale);
+    const double oy = dmul(-dadd(dadd(dmul(w0, U[0]), dmul(w1, U[1])), dmul(w2, U[2])), scale);
+    if (isfinite(ox) && isfinite(oy)) {
+        off[0] = ox;
+        off[1] = oy;
+    }
+}
+
+}  // namespace woit

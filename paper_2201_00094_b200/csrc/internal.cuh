@@ -1,0 +1,36 @@
+// Internal (C++) entry points shared between the .cu translation units.
+#pragma once
+
+#include "common.cuh"
+
+namespace woit {
+struct KParams;
+cudaError_t launch_frame(const KParams& kp, cudaStream_t st);
+cudaError_t launch_composite(const KParams& kp, cudaStream_t st);
+cudaError_t launch_indices(const KParams& kp, double* z, int32_t* k, int32_t* cells, cudaStream_t st);
+size_t bin_workspace(int64_t n, int64_t npix);
+cudaError_t bin_by_pixel(const int64_t* pix, int64_t n, int64_t npix, int64_t* offsets, int64_t* perm,
+                         void* ws, size_t ws_bytes, cudaStream_t st);
+size_t build_into_workspace(int64_t n, int64_t npix);
+cudaError_t build_into(double* coeffs, int64_t npix, const int64_t* pix, const double* z, const double* a,
+                       int64_t n, int rank, int mode, void* ws, size_t ws_bytes, cudaStream_t st);
+cudaError_t interp(const double* coeffs, const int64_t* pix, const double* z, int64_t n, int rank,
+                   double* out, cudaStream_t st);
+cudaError_t cells_raw(const double* coeffs, const int64_t* pix, const int64_t* cells, int64_t n, int rank,
+                      double* out, cudaStream_t st);
+cudaError_t total(const double* coeffs, int64_t npix, int rank, double* out, cudaStream_t st);
+cudaError_t pack(const double* v, int64_t n, uint32_t* words, cudaStream_t st);
+cudaError_t unpack(const uint32_t* words, int64_t n, double* out, cudaStream_t st);
+namespace synth {
+struct Out {
+    float *depth, *alpha, *trans, *rad, *normal, *ior;
+    uint8_t* bf;
+};
+size_t workspace(int64_t npix);
+cudaError_t offsets(int workload, int32_t width, uint32_t seed, int32_t layers, int32_t row0, int32_t rows,
+                    int64_t* off, void* ws, size_t ws_bytes, cudaStream_t st);
+cudaError_t fill(int workload, int32_t width, uint32_t seed, int32_t layers, int32_t row0, int32_t rows,
+                 const int64_t* off, int64_t nfrag_uniform, Out o, float* od, float* oc, cudaStream_t st);
+}  // namespace synth
+}  // namespace woit
+

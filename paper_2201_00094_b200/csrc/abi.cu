@@ -7,7 +7,7 @@ using namespace woit;
 
 namespace {
 
-constexpr int64_t kMinFB = 512;  // smallest sub-tile (rank 6): bounds the long-pixel list
+constexpr int64_t kMinFB = 256;  // smallest sub-tile (rank 6): bounds the long-pixel list
 
 int64_t long_cap(int64_t nfrag) { return nfrag / (kMinFB + 1) + 2; }
 

@@ -13,97 +13,25 @@
 
 namespace woit {
 
-template <int R>
-struct Smem {
-    int64_t* offs;
-    int64_t* nch;
-    int64_t* cb;
-    uint32_t* nearu;
-    uint32_t* faru;
-    double* lo;
-    double* den;
-    double* vtot;
-    uint32_t* chunk;
-    float* depth;
-    float* alpha;
-    float* trans;
-    float* rad;
-    float* ior;
-    float* normal;
-    uint8_t* bf;
-    int64_t* zfix;
-    float* r1;
-    unsigned char* r2;
-    uint64_t* bar;
-};
-
-template <int R>
-WOIT_D Smem<R> carve(unsigned char* base, const Layout& L) {
-    Smem<R> s;
-    s.offs = reinterpret_cast<int64_t*>(base + L.offs);
-    s.nch = reinterpret_cast<int64_t*>(base + L.nch);
-    s.cb = reinterpret_cast<int64_t*>(base + L.cb);
-    s.nearu = reinterpret_cast<uint32_t*>(base + L.nearu);
-    s.faru = reinterpret_cast<uint32_t*>(base + L.faru);
-    s.lo = reinterpret_cast<double*>(base + L.lo);
-    s.den = reinterpret_cast<double*>(base + L.den);
-    s.vtot = reinterpret_cast<double*>(base + L.vtot);
-    s.chunk = reinterpret_cast<uint32_t*>(base + L.chunk);
-    s.depth = reinterpret_cast<float*>(base + L.depth);
-    s.alpha = reinterpret_cast<float*>(base + L.alpha);
-    s.trans = reinterpret_cast<float*>(base + L.trans);
-    s.rad = reinterpret_cast<float*>(base + L.rad);
-    s.ior = reinterpret_cast<float*>(base + L.ior);
-    s.normal = reinterpret_cast<float*>(base + L.normal);
-    s.bf = reinterpret_cast<uint8_t*>(base + L.bf);
-    s.zfix = reinterpret_cast<int64_t*>(base + L.zfix);
-    s.r1 = reinterpret_cast<float*>(base + L.r1);
-    s.r2 = base + L.r2;
-    s.bar = reinterpret_cast<uint64_t*>(base + L.bar);
-    return s;
-}
-
-// chunk descriptor: pixel (7 bits), start within sub-tile (12 bits), length (5 bits)
+// chunk descriptor: pixel (8 bits), start within sub-tile (13 bits), length (5 bits)
 WOIT_D uint32_t pack_chunk(int q, int start, int len) {
-    return (uint32_t)q | ((uint32_t)start << 7) | ((uint32_t)len << 19);
+    return (uint32_t)q | ((uint32_t)start << 8) | ((uint32_t)len << 21);
 }
 WOIT_D void unpack_chunk(uint32_t c, int& q, int& start, int& len) {
-    q = (int)(c & 127u);
-    start = (int)((c >> 7) & 4095u);
-    len = (int)(c >> 19);
+    q = (int)(c & 255u);
+    start = (int)((c >> 8) & 8191u);
+    len = (int)(c >> 21);
 }
 
 // Within-chunk iteration starts at a rotation that depends only on the global
 // fragment id of the chunk start: it spreads the lanes of a warp over the 32
 // smem banks for uniform run lengths and keeps the summation order independent
 // of the tiling (bit-identical results for any band split).
-WOIT_D int chunk_rotation(int64_t gstart, int len) { return (int)((gstart >> 5) % len); }
+WOIT_D int chunk_rotation(int64_t gstart, int len) { return (int)((uint64_t)(gstart >> 5) % (uint64_t)len); }
 
 // rotation of the chunk loop in the per-pixel combine (same purpose)
-WOIT_D int combine_rotation(int64_t gpix, int64_t nch) { return (int)(((gpix * nch) >> 5) % nch); }
-
-// exclusive scan of one int64 per thread across the CTA (T threads)
-template <int T>
-WOIT_D int64_t block_exclusive_scan(int64_t v, int64_t* warp_sums, int64_t& total) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int64_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) warp_sums[wid] = x;
-    __syncthreads();
-    int64_t base = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < T / 32; ++w) {
-        const int64_t s = warp_sums[w];
-        base += (w < wid) ? s : 0;
-        tot += s;
-    }
-    total = tot;
-    __syncthreads();
-    return base + x - v;
+WOIT_D int combine_rotation(int64_t gpix, int nch) {
+    return (int)((uint64_t)((gpix * nch) >> 5) % (uint64_t)nch);
 }
 
 // ---------------------------------------------------------------------------
@@ -129,23 +57,13 @@ WOIT_D int64_t stage_bulk_end(const StageSpec& sp, int64_t fa, int64_t fb, int64
     return b > a ? b : a;
 }
 
-WOIT_D uint32_t stage_issue(const StageSpec& sp, int64_t fa, int64_t fb, int64_t nalloc,
-                            int use_tma, uint64_t* bar) {
-    int64_t a;
-    const int64_t e = stage_bulk_end(sp, fa, fb, nalloc, use_tma, a);
-    if (e <= a) return 0;
-    const uint32_t bytes = (uint32_t)((e - a) * sp.esize);
-    bulk_g2s(sp.s, static_cast<const unsigned char*>(sp.g) + a * sp.esize, bytes, bar);
-    return bytes;
-}
-
 template <int T>
-WOIT_D void stage_scalar(const StageSpec& sp, int64_t fa, int64_t fb, int64_t nalloc, int use_tma) {
+WOIT_D void stage_scalar(const StageSpec& sp, int64_t fa, int64_t fb, int64_t nalloc, int use_tma, int tid) {
     int64_t a;
     const int64_t e = stage_bulk_end(sp, fa, fb, nalloc, use_tma, a);
     const int64_t s0 = e > fa ? e : fa;
     const int words = sp.esize >= 4 ? sp.esize / 4 : 0;
-    for (int64_t i = s0 + threadIdx.x; i < fb; i += T) {
+    for (int64_t i = s0 + tid; i < fb; i += T) {
         if (words) {
             const float* g = static_cast<const float*>(sp.g) + i * words;
             float* d = static_cast<float*>(sp.s) + (i - a) * words;
@@ -156,62 +74,159 @@ WOIT_D void stage_scalar(const StageSpec& sp, int64_t fa, int64_t fb, int64_t na
     }
 }
 
-// ---------------------------------------------------------------------------
-
+// In-place inverse Haar synthesis of one channel: c[0..S) coefficients ->
+// staircase value at each of the M = S cell centres (wavelet.py:221-239),
+// level by level: cell(c) = c0 + sum_n 2^(n/2) (+/-) c[2^n + (c >> (N+1-n))].
 template <int R>
-__global__ void __launch_bounds__(RT<R>::T, 1) frame_kernel(const KParams kp) {
-    using G = RT<R>;
-    constexpr int T = G::T, PB = G::PB, FB = G::FB, V = G::V, S = G::S, CH = G::CH, VP = G::VP;
-    constexpr int M = S;
+WOIT_D void haar_cells(const double c[], double cell[]) {
+    constexpr int S = 1 << (R + 1);
+    cell[0] = c[0];
+    int width = 1;  // number of distinct values after level n-1
+#pragma unroll
+    for (int n = 0; n <= R; ++n) {
+        // each value splits into (v + s c, v - s c) with c = level-n offset k
+#pragma unroll
+        for (int k = (1 << n) - 1; k >= 0; --k) {
+            const double v = cell[k];
+            const double w = dmul(kSqrt2Pow[n], c[(1 << n) + k]);
+            cell[2 * k] = dadd(v, w);
+            cell[2 * k + 1] = dadd(v, -w);
+        }
+        width <<= 1;
+    }
+    (void)width;
+    (void)S;
+}
+
+// ---------------------------------------------------------------------------
+// The fused frame kernel. Every warp owns a window of WIN consecutive pixels and
+// processes it in sub-tiles of <= 32 chunks (<= 256 fragments) on its own slice
+// of shared memory, synchronising only with __syncwarp and its own mbarrier, so
+// warps never wait on each other. GEN=false is the compile-time fast path of the
+// fused frame without refraction / aberration / cubed transmission / packed
+// storage (the headline configuration); GEN=true covers every flag and the
+// step-wise entry points.
+
+template <int R, bool GEN>
+struct WSmem {
+    int64_t* offs;     // [WIN+1] window CSR offsets
+    int32_t* nch;      // [WIN]   chunks per pixel
+    int32_t* cb;       // [WIN+1] window chunk prefix
+    int32_t* rot;      // [WIN]   combine rotation
+    uint32_t* nearu;   // [WIN]   ordered-int near / far
+    uint32_t* faru;
+    double* lo;        // [WIN]   depth map
+    double* den;
+    double* rcp;
+    double* vtot;      // [WIN][3] exp(-A_total)
+    uint32_t* chunk;   // [32]   chunk descriptors
+    float* depth;      // staging [FBW+4] (granule-aligned window)
+    float* alpha;
+    float* trans;      // [FBW+4][3]
+    float* rad;        // [FBW+4][3], v̂ written in place
+    float* ior;
+    float* normal;
+    uint8_t* bf;
+    int64_t* zfix;     // [FBW] z in fixed point, by fragment
+    float* part;       // [V][32] chunk partials (f64 [WIN][V] scratch for packed storage)
+    float* cells;      // [WIN][V] staircase at cell centres
+    float* coef32;     // [WIN][V] coefficients, bulk-stored to bufs->coeffs
+    float* accp;       // [8][32] chunk accumulators
+    double* pk;        // [WIN][V] f64 coefficients for packed storage
+    uint64_t* bar;
+};
+
+template <int R, bool GEN>
+WOIT_D WSmem<R, GEN> wcarve(unsigned char* base, const WLayout& L) {
+    WSmem<R, GEN> s;
+    s.offs = reinterpret_cast<int64_t*>(base + L.offs);
+    s.nch = reinterpret_cast<int32_t*>(base + L.nch);
+    s.cb = reinterpret_cast<int32_t*>(base + L.cb);
+    s.rot = reinterpret_cast<int32_t*>(base + L.rot);
+    s.nearu = reinterpret_cast<uint32_t*>(base + L.nearu);
+    s.faru = reinterpret_cast<uint32_t*>(base + L.faru);
+    s.lo = reinterpret_cast<double*>(base + L.lo);
+    s.den = reinterpret_cast<double*>(base + L.den);
+    s.rcp = reinterpret_cast<double*>(base + L.rcp);
+    s.vtot = reinterpret_cast<double*>(base + L.vtot);
+    s.chunk = reinterpret_cast<uint32_t*>(base + L.chunk);
+    s.depth = reinterpret_cast<float*>(base + L.depth);
+    s.alpha = reinterpret_cast<float*>(base + L.alpha);
+    s.trans = reinterpret_cast<float*>(base + L.trans);
+    s.rad = reinterpret_cast<float*>(base + L.rad);
+    s.ior = reinterpret_cast<float*>(base + L.ior);
+    s.normal = reinterpret_cast<float*>(base + L.normal);
+    s.bf = reinterpret_cast<uint8_t*>(base + L.bf);
+    s.zfix = reinterpret_cast<int64_t*>(base + L.zfix);
+    s.part = reinterpret_cast<float*>(base + L.part);
+    s.cells = reinterpret_cast<float*>(base + L.cells);
+    s.coef32 = reinterpret_cast<float*>(base + L.coef32);
+    s.accp = reinterpret_cast<float*>(base + L.accp);
+    s.pk = reinterpret_cast<double*>(base + L.pk);
+    s.bar = reinterpret_cast<uint64_t*>(base + L.bar);
+    return s;
+}
+
+template <int R, bool GEN>
+__global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp) {
+    using G = WT<R>;
+    constexpr int S = G::S, V = G::V, CH = G::CH, WC = 32, FBW = G::FBW, WIN = G::WIN, SUBP = G::SUBP;
+    constexpr uint32_t kFused = PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const uint32_t ph = kp.phases;
-    const int flags = kp.p.flags;
-    const Layout L = make_layout<R>(ph, flags);
-    Smem<R> sm = carve<R>(smem_raw, L);
-    __shared__ int64_t warp_sums[T / 32];
+    const uint32_t ph = GEN ? kp.phases : kFused;
+    const int flags = GEN ? kp.p.flags : (kp.p.flags & WOIT_NORMALIZE);
+    const WLayout L = make_wlayout<R>(ph, flags);
+    const int lane = threadIdx.x & 31;
+    WSmem<R, GEN> sm = wcarve<R, GEN>(smem_raw + (threadIdx.x >> 5) * L.total, L);
 
-    const int tid = threadIdx.x;
-    const int64_t w0 = (int64_t)blockIdx.x * PB;
-    const int nq = (int)((kp.f.npix - w0) < PB ? (kp.f.npix - w0) : PB);
-    if (nq <= 0) return;
+    const int64_t w0 = ((int64_t)blockIdx.x * G::WPB + (threadIdx.x >> 5)) * WIN;
+    if (w0 >= kp.f.npix) return;  // warp-uniform
+    const int nq = (int)((kp.f.npix - w0) < WIN ? (kp.f.npix - w0) : WIN);
 
-    const bool do_frag = ph & (PH_BOUNDS | PH_BUILD | PH_EVAL);
     const bool do_at = ph & (PH_BUILD | PH_EVAL);
     const bool do_eval = ph & PH_EVAL;
-    const bool refr = do_eval && (flags & WOIT_REFRACTION);
-    const bool cube = flags & WOIT_CUBE_TRANSMISSION;
+    const bool need_coef = ph & (PH_EVAL | PH_COMPOSITE);
+    const bool refr = GEN && do_eval && (flags & WOIT_REFRACTION);
+    const bool cube = GEN && (flags & WOIT_CUBE_TRANSMISSION);
     const bool bfonly = cube && (flags & WOIT_CUBE_BACKFACE_ONLY);
     const bool need_ior = do_at && (cube || refr);
-    const bool keep_z = (ph & PH_BUILD) && do_eval;
+    const bool packed = GEN && (flags & WOIT_PACKED_STORAGE);
     const int64_t nalloc = kp.f.nfrag;
 
-    if (tid == 0) mbar_init(sm.bar, 1);
-    for (int q = tid; q <= nq; q += T) sm.offs[q] = kp.f.offsets[w0 + q];
-    __syncthreads();
-    // chunks per pixel and their window prefix
-    int64_t my_nch = 0;
-    if (tid < nq) {
-        const int64_t run = sm.offs[tid + 1] - sm.offs[tid];
-        my_nch = (run + CH - 1) / CH;
-        sm.nch[tid] = my_nch;
+    if (lane == 0) mbar_init(sm.bar, 1);
+    if (lane <= nq) sm.offs[lane] = kp.f.offsets[w0 + lane];
+    if (lane == 0 && nq == 32) sm.offs[32] = kp.f.offsets[w0 + 32];
+    __syncwarp();
+    // chunks per pixel, window prefix (warp scan) and combine rotation
+    int my_nch = 0;
+    if (lane < nq) {
+        const int64_t run = sm.offs[lane + 1] - sm.offs[lane];
+        const int64_t nc64 = (run + CH - 1) / CH;
+        my_nch = nc64 > (1 << 24) ? (1 << 24) : (int)nc64;  // long pixels never form a sub-tile
+        sm.nch[lane] = my_nch;
+        sm.rot[lane] = my_nch > 0 ? combine_rotation(kp.f.pixel_base + w0 + lane, my_nch) : 0;
     }
-    int64_t tot;
-    const int64_t ex = block_exclusive_scan<T>(my_nch, warp_sums, tot);
-    if (tid < nq) sm.cb[tid] = ex;
-    if (tid == 0) sm.cb[nq] = tot;
-    __syncthreads();
+    int inc = my_nch;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane < nq) sm.cb[lane + 1] = inc;
+    if (lane == 0) sm.cb[0] = 0;
+    __syncwarp();
 
     uint32_t parity = 0;
     int q0 = 0;
     while (q0 < nq) {
-        // sub-tile end: largest q1 with <= FB fragments and <= T chunks
-        const int cand = tid + 1;
-        const bool fits = cand > q0 && cand <= nq && (sm.offs[cand] - sm.offs[q0]) <= FB &&
-                          (sm.cb[cand] - sm.cb[q0]) <= T;
-        const int cnt = __syncthreads_count(fits);
+        // sub-tile end: largest q1 with <= FBW fragments and <= 32 chunks
+        const int cand = lane + 1;
+        const bool fits = cand > q0 && cand <= nq && cand - q0 <= SUBP &&
+                          (sm.offs[cand] - sm.offs[q0]) <= FBW && (sm.cb[cand] - sm.cb[q0]) <= WC;
+        const int cnt = __popc(__ballot_sync(0xffffffffu, fits));
         if (cnt == 0) {
-            // a single pixel deeper than FB fragments: handled by long_pixel_kernel
-            if (tid == 0) {
+            // a single pixel deeper than FBW fragments: handled by long_pixel_kernel
+            if (lane == 0) {
                 const unsigned long long idx =
                     atomicAdd(reinterpret_cast<unsigned long long*>(kp.long_list), 1ull);
                 if ((int64_t)idx < kp.long_cap) kp.long_list[1 + idx] = w0 + q0;
@@ -222,126 +237,136 @@ __global__ void __launch_bounds__(RT<R>::T, 1) frame_kernel(const KParams kp) {
         const int q1 = q0 + cnt;
         const int nqs = q1 - q0;
         const int64_t fa = sm.offs[q0], fb = sm.offs[q1];
-        const int C = (int)(sm.cb[q1] - sm.cb[q0]);
+        const int C = sm.cb[q1] - sm.cb[q0];
         const int64_t a4 = fa & ~(int64_t)3, a16 = fa & ~(int64_t)15;
         const int sh4 = (int)(fa - a4);  // staging index of fragment fa (granule-4 arrays)
+        const int shb = (int)(fa - a16);
 
-        // ---- 1. stage fragment fields (TMA bulk) ---------------------------------
-        StageSpec specs[7];
-        int nspec = 0;
-        if (do_frag) specs[nspec++] = {kp.f.depth, sm.depth, 4, 4};
-        if (do_at) specs[nspec++] = {kp.f.alpha, sm.alpha, 4, 4};
-        if (do_at) specs[nspec++] = {kp.f.trans, sm.trans, 12, 4};
-        if (do_eval) specs[nspec++] = {kp.f.radiance, sm.rad, 12, 4};
-        if (need_ior && kp.f.ior) specs[nspec++] = {kp.f.ior, sm.ior, 4, 4};
-        if (refr) specs[nspec++] = {kp.f.normal, sm.normal, 12, 4};
-        if (bfonly && kp.f.backface) specs[nspec++] = {kp.f.backface, sm.bf, 1, 16};
-        if (kp.use_tma && nspec > 0 && tid == 0) {
-            bulk_wait_read_all();  // previous sub-tile's v̂ store has left smem
-            fence_proxy_async();
-            uint32_t tx = 0;
-            for (int i = 0; i < nspec; ++i) {
-                int64_t a;
-                const int64_t e = stage_bulk_end(specs[i], fa, fb, nalloc, 1, a);
-                if (e > a) tx += (uint32_t)((e - a) * specs[i].esize);
+        // ---- 1. stage fragment fields (TMA bulk copies, one mbarrier per warp) ----
+        {
+            StageSpec specs[7];
+            int nspec = 0;
+            specs[nspec++] = {kp.f.depth, sm.depth, 4, 4};
+            if (do_at) specs[nspec++] = {kp.f.alpha, sm.alpha, 4, 4};
+            if (do_at) specs[nspec++] = {kp.f.trans, sm.trans, 12, 4};
+            if (do_eval) specs[nspec++] = {kp.f.radiance, sm.rad, 12, 4};
+            if (GEN && need_ior && kp.f.ior) specs[nspec++] = {kp.f.ior, sm.ior, 4, 4};
+            if (GEN && refr) specs[nspec++] = {kp.f.normal, sm.normal, 12, 4};
+            if (GEN && bfonly && kp.f.backface) specs[nspec++] = {kp.f.backface, sm.bf, 1, 16};
+            if (kp.use_tma && lane == 0) {
+                bulk_wait_read_all();  // the previous sub-tile's stores have left smem
+                uint32_t tx = 0;
+                for (int i = 0; i < nspec; ++i) {
+                    int64_t a;
+                    const int64_t e = stage_bulk_end(specs[i], fa, fb, nalloc, 1, a);
+                    if (e > a) tx += (uint32_t)((e - a) * specs[i].esize);
+                }
+                mbar_arrive_expect_tx(sm.bar, tx);
+                for (int i = 0; i < nspec; ++i) {
+                    int64_t a;
+                    const int64_t e = stage_bulk_end(specs[i], fa, fb, nalloc, 1, a);
+                    if (e > a)
+                        bulk_g2s(specs[i].s, static_cast<const unsigned char*>(specs[i].g) + a * specs[i].esize,
+                                 (uint32_t)((e - a) * specs[i].esize), sm.bar);
+                }
             }
-            mbar_arrive_expect_tx(sm.bar, tx);
-            for (int i = 0; i < nspec; ++i) stage_issue(specs[i], fa, fb, nalloc, 1, sm.bar);
+            for (int i = 0; i < nspec; ++i) stage_scalar<32>(specs[i], fa, fb, nalloc, kp.use_tma, lane);
+            if (GEN && need_ior && !kp.f.ior)
+                for (int i = lane; i < (int)(fb - fa); i += 32) sm.ior[sh4 + i] = 1.0f;
+            if (GEN && bfonly && !kp.f.backface)
+                for (int i = lane; i < (int)(fb - fa); i += 32) sm.bf[shb + i] = 0;
         }
-        for (int i = 0; i < nspec; ++i) stage_scalar<T>(specs[i], fa, fb, nalloc, kp.use_tma);
-        if (need_ior && !kp.f.ior)
-            for (int i = tid; i < (int)(fb - fa); i += T) sm.ior[sh4 + i] = 1.0f;
-        if (bfonly && !kp.f.backface)
-            for (int i = tid; i < (int)(fb - fa); i += T) sm.bf[(int)(fa - a16) + i] = 0;
 
         // ---- 2. chunk table + per-pixel init (overlaps the copies) -----------------
-        if (tid < nqs) {
-            const int q = q0 + tid;
-            const int64_t run = sm.offs[q + 1] - sm.offs[q];
-            const int nc = (int)sm.nch[q];
-            const int base = (int)(sm.cb[q] - sm.cb[q0]);
+        float bgc[3] = {0.f, 0.f, 0.f};
+        if (lane < nqs) {
+            const int q = q0 + lane;
+            const int run = (int)(sm.offs[q + 1] - sm.offs[q]);
+            const int nc = sm.nch[q];
+            const int base = sm.cb[q] - sm.cb[q0];
             const int rel = (int)(sm.offs[q] - fa);
             if (nc > 0) {
-                const int len0 = (int)(run / nc), extra = (int)(run % nc);
+                const int len0 = run / nc, extra = run - len0 * nc;
                 int st = rel;
                 for (int i = 0; i < nc; ++i) {
                     const int len = len0 + (i < extra ? 1 : 0);
-                    sm.chunk[base + i] = pack_chunk(tid, st, len);
+                    sm.chunk[base + i] = pack_chunk(lane, st, len);
                     st += len;
                 }
             }
             const int64_t p = w0 + q;
-            if (ph & PH_BOUNDS) {
-                if (ph & PH_BOUNDS_ACC) {
-                    sm.nearu[tid] = f2ord(kp.b.near[p]);
-                    sm.faru[tid] = f2ord(kp.b.far[p]);
-                } else {
-                    sm.nearu[tid] = f2ord(INFINITY);
-                    sm.faru[tid] = f2ord(-INFINITY);
-                }
-            } else {
-                sm.nearu[tid] = f2ord(kp.b.near[p]);
-                sm.faru[tid] = f2ord(kp.b.far[p]);
+            if (!GEN) {  // background of the composite, fetched early to hide its latency
+                bgc[0] = kp.f.opaque_color[p * 3];
+                bgc[1] = kp.f.opaque_color[p * 3 + 1];
+                bgc[2] = kp.f.opaque_color[p * 3 + 2];
             }
+            const bool init_empty = (ph & PH_BOUNDS) && !(ph & PH_BOUNDS_ACC);
+            sm.nearu[lane] = f2ord(init_empty ? INFINITY : kp.b.near[p]);
+            sm.faru[lane] = f2ord(init_empty ? -INFINITY : kp.b.far[p]);
         }
-        if (kp.use_tma && nspec > 0) {
+        if (kp.use_tma) {
             mbar_wait(sm.bar, parity);
             parity ^= 1u;
         }
-        __syncthreads();
+        __syncwarp();
+
+        // this lane's chunk (lanes >= C idle in the fragment phases)
+        int cq = 0, cst = 0, clen = 0, crot = 0;
+        if (lane < C) {
+            unpack_chunk(sm.chunk[lane], cq, cst, clen);
+            crot = chunk_rotation(kp.f.frag_base + fa + cst, clen);
+        }
 
         // ---- 3. bounds (step1) ------------------------------------------------------
         if (ph & PH_BOUNDS) {
-            if (tid < C) {
-                int q, st, len;
-                unpack_chunk(sm.chunk[tid], q, st, len);
+            if (lane < C) {
                 float mn = INFINITY, mx = -INFINITY;
-                for (int j = 0; j < len; ++j) {
-                    const float x = sm.depth[sh4 + st + j];
+                for (int j = 0; j < clen; ++j) {
+                    const float x = sm.depth[sh4 + cst + j];
                     mn = fminf(mn, x);
                     mx = fmaxf(mx, x);
                 }
-                atomicMin(&sm.nearu[q], f2ord(mn));
-                atomicMax(&sm.faru[q], f2ord(mx));
+                atomicMin(&sm.nearu[cq], f2ord(mn));
+                atomicMax(&sm.faru[cq], f2ord(mx));
             }
-            __syncthreads();
+            __syncwarp();
         }
-        if (tid < nqs) {
-            const float nf = ord2f(sm.nearu[tid]), ff = ord2f(sm.faru[tid]);
-            const int64_t p = w0 + q0 + tid;
+        if (lane < nqs) {
+            const float nf = ord2f(sm.nearu[lane]), ff = ord2f(sm.faru[lane]);
+            const int64_t p = w0 + q0 + lane;
             if ((ph & PH_BOUNDS) && kp.b.near) kp.b.near[p] = nf;
             if ((ph & PH_BOUNDS) && kp.b.far) kp.b.far[p] = ff;
             const DepthMap m = depth_map(nf, ff, R);
-            sm.lo[tid] = m.lo;
-            sm.den[tid] = m.den;
+            sm.lo[lane] = m.lo;
+            sm.den[lane] = m.den;
+            sm.rcp[lane] = m.rcp;
         }
-        __syncthreads();
+        __syncwarp();
 
-        // ---- 4. build (step2): chunk partials -> r1[v][c] --------------------------
-        float* part = sm.r1;
-        double* coef64 = reinterpret_cast<double*>(sm.r2);
+        // ---- 4. z (fixed point) and build (step2): chunk partials -> part[v][lane] ----
+        float* part = sm.part;
+        if (lane < C && do_at) {
+            const DepthMap m{sm.lo[cq], sm.den[cq], sm.rcp[cq]};
+            for (int j = 0; j < clen; ++j) {
+                const int fr = cst + j;
+                sm.zfix[fr] = z_fixed(normalized_z(sm.depth[sh4 + fr], m));
+            }
+        }
         if (ph & PH_BUILD) {
-            if (tid < C) {
-                int q, st, len;
-                unpack_chunk(sm.chunk[tid], q, st, len);
-                const DepthMap m{sm.lo[q], sm.den[q]};
-                for (int v = 6; v < V; ++v) part[v * T + tid] = 0.0f;
+            if (lane < C) {
+#pragma unroll
+                for (int v = 6; v < V; ++v) part[v * WC + lane] = 0.0f;
                 float s0[3] = {0.f, 0.f, 0.f}, s1[3] = {0.f, 0.f, 0.f};
-                const int rot = chunk_rotation(kp.f.frag_base + fa + st, len);
-                for (int j = 0; j < len; ++j) {
-                    int jj = j + rot;
-                    if (jj >= len) jj -= len;
-                    const int fr = st + jj;          // fragment index relative to fa
-                    const int si = sh4 + fr;         // staging index
-                    const double z = normalized_z(sm.depth[si], m);
-                    const int64_t zi = z_fixed(z);
-                    if (keep_z) sm.zfix[fr] = zi;
+                int jj = crot;
+#pragma unroll 1
+                for (int j = 0; j < clen; ++j) {
+                    const int fr = cst + jj;   // fragment index relative to fa
+                    jj = jj + 1 == clen ? 0 : jj + 1;
+                    const int si = sh4 + fr;   // staging index
+                    const int64_t zi = sm.zfix[fr];
                     const float al = sm.alpha[si];
                     bool cb_ = false;
-                    if (cube) {
-                        const float io = sm.ior[si];
-                        cb_ = io > 1.0f && (!bfonly || sm.bf[(int)(fa - a16) + fr] != 0);
-                    }
+                    if (cube) cb_ = sm.ior[si] > 1.0f && (!bfonly || sm.bf[shb + fr] != 0);
                     float a[3];
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) a[ch] = absorbance_ch(al, sm.trans[3 * si + ch], cb_);
@@ -356,132 +381,169 @@ __global__ void __launch_bounds__(RT<R>::T, 1) frame_kernel(const KParams kp) {
                     for (int n = 1; n <= R; ++n) {
                         const int k = slot_offset(zi, n);
                         const float psi = level_psi(zi, n) * kInvSqrt2PowF[n];
-                        float* col = part + ((1 << n) + k) * 3 * T + tid;
+                        float* col = part + ((1 << n) + k) * 3 * WC + lane;
 #pragma unroll
-                        for (int ch = 0; ch < 3; ++ch) col[ch * T] -= a[ch] * psi;
+                        for (int ch = 0; ch < 3; ++ch) col[ch * WC] -= a[ch] * psi;
                     }
                 }
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) {
-                    part[ch * T + tid] = s0[ch];
-                    part[(3 + ch) * T + tid] = s1[ch];
+                    part[ch * WC + lane] = s0[ch];
+                    part[(3 + ch) * WC + lane] = s1[ch];
                 }
             }
-            __syncthreads();
-            // combine chunk partials per (pixel, value) in fp64, fixed order
-            for (int idx = tid; idx < nqs * V; idx += T) {
-                const int v = idx / nqs, ql = idx - v * nqs;
-                const int q = q0 + ql;
-                const int64_t nc = sm.nch[q];
-                const int cbq = (int)(sm.cb[q] - sm.cb[q0]);
-                double acc = (ph & PH_BUILD_ACC) ? (double)kp.b.coeffs[(w0 + q) * V + v] : 0.0;
-                if (nc > 0) {
-                    const int r = combine_rotation(kp.f.pixel_base + w0 + q, nc);
-                    const float* pv = part + v * T + cbq;
-                    for (int i = 0; i < nc; ++i) {
-                        int ii = i + r;
-                        if (ii >= nc) ii -= (int)nc;
-                        acc += (double)pv[ii];
-                    }
-                }
-                coef64[ql * VP + v] = acc;
-            }
-            __syncthreads();
-            if (flags & WOIT_PACKED_STORAGE) {
-                for (int idx = tid; idx < nqs * S; idx += T) {
-                    const int ql = idx / S, s = idx - ql * S;
-                    double* c = coef64 + ql * VP + 3 * s;
-                    double mag[3] = {fabs(c[0]), fabs(c[1]), fabs(c[2])}, rt[3];
-                    rgb9e5_unpack_impl(rgb9e5_pack_impl(mag), rt);
-                    const double sg = s == 0 ? 1.0 : -1.0;
-                    c[0] = sg * rt[0];
-                    c[1] = sg * rt[1];
-                    c[2] = sg * rt[2];
-                }
-                __syncthreads();
-            }
-            if (kp.b.coeffs) {
-                for (int idx = tid; idx < nqs * V; idx += T) {
-                    const int ql = idx / V, v = idx - ql * V;
-                    kp.b.coeffs[(w0 + q0) * V + idx] = (float)coef64[ql * VP + v];
-                }
-            }
-        } else if (ph & (PH_EVAL | PH_COMPOSITE)) {
-            for (int idx = tid; idx < nqs * V; idx += T) {
-                const int ql = idx / V, v = idx - ql * V;
-                coef64[ql * VP + v] = (double)kp.b.coeffs[(w0 + q0) * V + idx];
-            }
-            __syncthreads();
+            __syncwarp();
         }
 
-        // ---- 5. per-pixel total transmittance and cell staircase ------------------
-        float* cells = sm.r1;  // r1 is free again (partials consumed)
-        if (ph & (PH_EVAL | PH_COMPOSITE)) {
-            for (int idx = tid; idx < nqs * 3; idx += T) {
-                const int ql = idx / 3, ch = idx - ql * 3;
-                const double* c = coef64 + ql * VP;
-                double at = c[ch];
+        // ---- 5. per (pixel, channel): combine chunks in f64, coefficients, total
+        //         transmittance and the cell staircase --------------------------------
+        if (ph & PH_BUILD) {
+            // pixel fastest across lanes: the rotated chunk reads hit distinct banks.
+            // nqs <= SUBP keeps this to one round, so every lane has read its partials
+            // before the region is reused for coefficients and cells.
+            const int t = lane;
+            const bool task = t < nqs * 3;
+            const int kch = task ? t / nqs : 0, kq = task ? t - kch * nqs : 0;
+            double c[S];
+            if (task) {
+                const int q = q0 + kq;
+                const int nc = sm.nch[q];
+                const int cbq = sm.cb[q] - sm.cb[q0];
+                const int r = sm.rot[q];
+                const float* pv = part + kch * WC + cbq;
 #pragma unroll
-                for (int n = 0; n <= R; ++n) at = dsub(at, dmul(kSqrt2Pow[n], c[((2 << n) - 1) * 3 + ch]));
-                sm.vtot[idx] = exp(-fmax(at, 0.0));
-            }
-            if (do_eval) {
-                for (int idx = tid; idx < nqs * V; idx += T) {
-                    const int ql = idx / V, w = idx - ql * V;
-                    const int cell = w / 3, ch = w - cell * 3;
-                    const double* c = coef64 + ql * VP;
-                    double val = c[ch];
+                for (int s = 0; s < S; ++s)
+                    c[s] = (GEN && (ph & PH_BUILD_ACC)) ? (double)kp.b.coeffs[(w0 + q) * V + 3 * s + kch] : 0.0;
+                int ii = r;
+#pragma unroll 1
+                for (int i = 0; i < nc; ++i) {
 #pragma unroll
-                    for (int n = 0; n <= R; ++n) {
-                        const int mm = R + 1 - n;
-                        const double sg = ((cell >> (mm - 1)) & 1) ? -1.0 : 1.0;
-                        val = dadd(val, dmul(dmul(kSqrt2Pow[n], sg), c[((1 << n) + (cell >> mm)) * 3 + ch]));
-                    }
-                    cells[idx] = (float)val;
+                    for (int s = 0; s < S; ++s) c[s] += (double)pv[s * 3 * WC + ii];
+                    ii = ii + 1 == nc ? 0 : ii + 1;
                 }
             }
-            __syncthreads();
+            __syncwarp();
+            if (!packed && task) {
+#pragma unroll
+                for (int s = 0; s < S; ++s) sm.coef32[kq * V + 3 * s + kch] = (float)c[s];
+                if (need_coef) {
+                    double at = c[0];
+#pragma unroll
+                    for (int n = 0; n <= R; ++n) at = dsub(at, dmul(kSqrt2Pow[n], c[(2 << n) - 1]));
+                    sm.vtot[kq * 3 + kch] = exp(-fmax(at, 0.0));
+                }
+                if (do_eval) {
+                    double cell[S];
+                    haar_cells<R>(c, cell);
+#pragma unroll
+                    for (int s = 0; s < S; ++s) sm.cells[kq * V + 3 * s + kch] = (float)cell[s];
+                }
+            }
+            if (GEN && packed && task) {
+                // the shared exponent couples the channels: stage the f64 coefficients
+#pragma unroll
+                for (int s = 0; s < S; ++s) sm.pk[kq * V + 3 * s + kch] = c[s];
+            }
+            if (GEN && packed) {
+                __syncwarp();
+                double* c64 = sm.pk;
+                for (int idx = lane; idx < nqs * S; idx += 32) {
+                    double* t3 = c64 + idx * 3;
+                    double mag[3] = {fabs(t3[0]), fabs(t3[1]), fabs(t3[2])}, rt[3];
+                    rgb9e5_unpack_impl(rgb9e5_pack_impl(mag), rt);
+                    const double sg = (idx % S) == 0 ? 1.0 : -1.0;
+                    t3[0] = sg * rt[0];
+                    t3[1] = sg * rt[1];
+                    t3[2] = sg * rt[2];
+                }
+                __syncwarp();
+                for (int t = lane; t < nqs * 3; t += 32) {
+                    const int kch = t / nqs, kq = t - kch * nqs;
+                    double c[S];
+#pragma unroll
+                    for (int s = 0; s < S; ++s) c[s] = c64[kq * V + 3 * s + kch];
+#pragma unroll
+                    for (int s = 0; s < S; ++s) sm.coef32[kq * V + 3 * s + kch] = (float)c[s];
+                    if (need_coef) {
+                        double at = c[0];
+#pragma unroll
+                        for (int n = 0; n <= R; ++n) at = dsub(at, dmul(kSqrt2Pow[n], c[(2 << n) - 1]));
+                        sm.vtot[kq * 3 + kch] = exp(-fmax(at, 0.0));
+                    }
+                    if (do_eval) {
+                        double cell[S];
+                        haar_cells<R>(c, cell);
+#pragma unroll
+                        for (int s = 0; s < S; ++s) sm.cells[kq * V + 3 * s + kch] = (float)cell[s];
+                    }
+                }
+            }
+        } else if (GEN && need_coef) {
+            for (int t = lane; t < nqs * 3; t += 32) {
+                const int kch = t / nqs, kq = t - kch * nqs;
+                const int64_t p = w0 + q0 + kq;
+                double c[S];
+#pragma unroll
+                for (int s = 0; s < S; ++s) c[s] = (double)kp.b.coeffs[p * V + 3 * s + kch];
+                double at = c[0];
+#pragma unroll
+                for (int n = 0; n <= R; ++n) at = dsub(at, dmul(kSqrt2Pow[n], c[(2 << n) - 1]));
+                sm.vtot[kq * 3 + kch] = exp(-fmax(at, 0.0));
+                double cell[S];
+                haar_cells<R>(c, cell);
+#pragma unroll
+                for (int s = 0; s < S; ++s) sm.cells[kq * V + 3 * s + kch] = (float)cell[s];
+            }
+        }
+        fence_proxy_async();  // coef32 becomes visible to the bulk store
+        __syncwarp();
+        if ((ph & PH_BUILD) && kp.b.coeffs) {
+            float* g = kp.b.coeffs + (w0 + q0) * V;
+            const uint32_t bytes = (uint32_t)(nqs * V * 4);
+            if (kp.use_tma && ((reinterpret_cast<uintptr_t>(g) & 15u) == 0) && (bytes & 15u) == 0) {
+                if (lane == 0) {
+                    bulk_s2g(g, sm.coef32, bytes);
+                    bulk_commit();
+                }
+            } else {
+                for (int i = lane; i < nqs * V; i += 32) g[i] = sm.coef32[i];
+            }
         }
 
         // ---- 6. evaluate (step3): v̂ per fragment, chunk accumulators --------------
-        float* accp = reinterpret_cast<float*>(sm.r2);  // [8][T], coef64 consumed
         if (do_eval) {
-            if (tid < C) {
-                int q, st, len;
-                unpack_chunk(sm.chunk[tid], q, st, len);
-                const DepthMap m{sm.lo[q], sm.den[q]};
-                const float* cq = cells + q * V;
+            if (lane < C) {
+                const float* cqv = sm.cells + cq * V;
                 float ac[3] = {0.f, 0.f, 0.f}, wg[3] = {0.f, 0.f, 0.f};
                 double ro[2] = {0.0, 0.0};
                 double d[3] = {0.0, 0.0, 0.0}, topq = INFINITY;
-                const int64_t p = w0 + q0 + q;
+                const int64_t p = w0 + q0 + cq;
                 if (refr) {
                     ray_dir(kp, kp.f.pixel_base + p, d);
                     topq = kp.f.opaque_depth ? (double)kp.f.opaque_depth[p] : INFINITY;
                 }
-                const int rot = chunk_rotation(kp.f.frag_base + fa + st, len);
-                for (int j = 0; j < len; ++j) {
-                    int jj = j + rot;
-                    if (jj >= len) jj -= len;
-                    const int fr = st + jj;
+                int jj = crot;
+#pragma unroll 1
+                for (int j = 0; j < clen; ++j) {
+                    const int fr = cst + jj;
+                    jj = jj + 1 == clen ? 0 : jj + 1;
                     const int si = sh4 + fr;
-                    const int64_t zi = keep_z ? sm.zfix[fr] : z_fixed(normalized_z(sm.depth[si], m));
                     int c0, c1;
                     float t;
-                    eval_cells(zi, R, c0, c1, t);
+                    eval_cells(sm.zfix[fr], R, c0, c1, t);
                     const float al = sm.alpha[si];
                     bool cb_ = false;
                     float io = 1.0f;
                     if (need_ior) {
                         io = sm.ior[si];
-                        cb_ = cube && io > 1.0f && (!bfonly || sm.bf[(int)(fa - a16) + fr] != 0);
+                        cb_ = cube && io > 1.0f && (!bfonly || sm.bf[shb + fr] != 0);
                     }
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) {
-                        const float A = fmaxf((1.0f - t) * cq[c0 * 3 + ch] + t * cq[c1 * 3 + ch], 0.0f);
-                        const float vh = expf(-A);
-                        const float L = sm.rad[3 * si + ch];
-                        ac[ch] += (L * al) * vh;
+                        const float A = fmaxf((1.0f - t) * cqv[c0 * 3 + ch] + t * cqv[c1 * 3 + ch], 0.0f);
+                        const float vh = __expf(-A);
+                        const float Lr = sm.rad[3 * si + ch];
+                        ac[ch] += (Lr * al) * vh;
                         wg[ch] += opacity_ch(al, sm.trans[3 * si + ch], cb_) * vh;
                         sm.rad[3 * si + ch] = vh;  // v̂ replaces radiance in place
                     }
@@ -495,23 +557,23 @@ __global__ void __launch_bounds__(RT<R>::T, 1) frame_kernel(const KParams kp) {
                 }
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) {
-                    accp[ch * T + tid] = ac[ch];
-                    accp[(3 + ch) * T + tid] = wg[ch];
+                    sm.accp[ch * WC + lane] = ac[ch];
+                    sm.accp[(3 + ch) * WC + lane] = wg[ch];
                 }
-                accp[6 * T + tid] = (float)ro[0];
-                accp[7 * T + tid] = (float)ro[1];
+                sm.accp[6 * WC + lane] = (float)ro[0];
+                sm.accp[7 * WC + lane] = (float)ro[1];
             }
             fence_proxy_async();  // v̂ in smem becomes visible to the bulk store
-            __syncthreads();
-            // v̂ store: aligned interior by one bulk copy, ragged ends by threads
+            __syncwarp();
+            // v̂ store: aligned interior by one bulk copy, ragged ends by the lanes
             if (kp.b.vhat) {
                 const int64_t i0 = (fa + 3) & ~(int64_t)3, i1 = fb & ~(int64_t)3;
                 const bool bulk = kp.use_tma && i1 > i0;
-                if (bulk && tid == 0) {
+                if (bulk && lane == 0) {
                     bulk_s2g(kp.b.vhat + 3 * i0, sm.rad + 3 * (i0 - a4), (uint32_t)(12 * (i1 - i0)));
                     bulk_commit();
                 }
-                for (int64_t f = fa + tid; f < fb; f += T) {
+                for (int64_t f = fa + lane; f < fb; f += 32) {
                     if (bulk && f >= i0 && f < i1) continue;
                     const int si = (int)(f - a4);
                     kp.b.vhat[3 * f] = sm.rad[3 * si];
@@ -522,11 +584,11 @@ __global__ void __launch_bounds__(RT<R>::T, 1) frame_kernel(const KParams kp) {
         }
 
         // ---- 7. per-pixel accumulators + composite (step4) -------------------------
-        if (tid < nqs) {
-            const int q = q0 + tid;
+        if (lane < nqs) {
+            const int q = q0 + lane;
             const int64_t p = w0 + q;
             double acc[3] = {0, 0, 0}, wgt[3] = {0, 0, 0}, ro[2] = {0, 0};
-            const bool acc_in = (ph & PH_EVAL_ACC) || ((ph & PH_COMPOSITE) && !do_eval);
+            const bool acc_in = GEN && ((ph & PH_EVAL_ACC) || ((ph & PH_COMPOSITE) && !do_eval));
             if (acc_in) {
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) {
@@ -539,17 +601,19 @@ __global__ void __launch_bounds__(RT<R>::T, 1) frame_kernel(const KParams kp) {
                 }
             }
             if (do_eval) {
-                const int64_t nc = sm.nch[q];
-                const int cbq = (int)(sm.cb[q] - sm.cb[q0]);
+                const int nc = sm.nch[q];
+                const int cbq = sm.cb[q] - sm.cb[q0];
                 for (int i = 0; i < nc; ++i) {
-                    const int c = cbq + i;
+                    const int cc = cbq + i;
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) {
-                        acc[ch] += (double)accp[ch * T + c];
-                        wgt[ch] += (double)accp[(3 + ch) * T + c];
+                        acc[ch] += (double)sm.accp[ch * WC + cc];
+                        wgt[ch] += (double)sm.accp[(3 + ch) * WC + cc];
                     }
-                    ro[0] += (double)accp[6 * T + c];
-                    ro[1] += (double)accp[7 * T + c];
+                    if (refr) {
+                        ro[0] += (double)sm.accp[6 * WC + cc];
+                        ro[1] += (double)sm.accp[7 * WC + cc];
+                    }
                 }
                 if (kp.b.accum)
                     for (int ch = 0; ch < 3; ++ch) kp.b.accum[p * 3 + ch] = (float)acc[ch];
@@ -562,15 +626,20 @@ __global__ void __launch_bounds__(RT<R>::T, 1) frame_kernel(const KParams kp) {
             }
             if ((ph & PH_COMPOSITE) && kp.b.output) {
                 float out[3];
-                composite_pixel(kp, p, acc, wgt, ro[0], ro[1], sm.vtot + 3 * tid, out);
+                if (GEN) {
+                    composite_pixel(kp, p, acc, wgt, ro[0], ro[1], sm.vtot + 3 * lane, out);
+                } else {
+                    composite_plain(flags, bgc, acc, wgt, sm.vtot + 3 * lane, out);
+                }
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) kp.b.output[p * 3 + ch] = out[ch];
             }
         }
-        __syncthreads();
+        fence_proxy_async();
+        __syncwarp();
         q0 = q1;
     }
-    if (tid == 0) bulk_wait_all();
+    if (lane == 0) bulk_wait_all();
 }
 
 // ---------------------------------------------------------------------------
@@ -778,23 +847,34 @@ size_t long_smem_bytes() {
     return (size_t)V * TL * 8 + (size_t)V * 8 + (size_t)V * 4;
 }
 
+template <int R, bool GEN>
+cudaError_t launch_tiles(const KParams& kp, cudaStream_t st) {
+    using G = WT<R>;
+    const uint32_t ph = GEN ? kp.phases : (PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE);
+    const WLayout L = make_wlayout<R>(ph, GEN ? kp.p.flags : (kp.p.flags & WOIT_NORMALIZE));
+    const int bytes = (int)(L.total * G::WPB);
+    cudaError_t err = cudaFuncSetAttribute(frame_kernel<R, GEN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (err != cudaSuccess) return err;
+    const int64_t warps = (kp.f.npix + G::WIN - 1) / G::WIN;
+    const int64_t grid = (warps + G::WPB - 1) / G::WPB;
+    if (grid > 0) {
+        frame_kernel<R, GEN><<<(unsigned)grid, G::WPB * 32, bytes, st>>>(kp);
+        err = cudaGetLastError();
+    }
+    return err;
+}
+
 template <int R>
 cudaError_t launch_rank(const KParams& kp, cudaStream_t st) {
-    using G = RT<R>;
-    const Layout L = make_layout<R>(kp.phases, kp.p.flags);
-    cudaError_t err = cudaFuncSetAttribute(frame_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)L.total);
+    using G = WT<R>;
+    constexpr uint32_t kFused = PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE;
+    const bool fast = kp.phases == kFused && (kp.p.flags & ~WOIT_NORMALIZE) == 0;
+    cudaError_t err = fast ? launch_tiles<R, false>(kp, st) : launch_tiles<R, true>(kp, st);
     if (err != cudaSuccess) return err;
-    const int64_t grid = (kp.f.npix + G::PB - 1) / G::PB;
-    if (grid > 0) {
-        frame_kernel<R><<<(unsigned)grid, G::T, L.total, st>>>(kp);
-        err = cudaGetLastError();
-        if (err != cudaSuccess) return err;
-    }
     const size_t ls = long_smem_bytes<R>();
     err = cudaFuncSetAttribute(long_pixel_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ls);
     if (err != cudaSuccess) return err;
-    if (kp.f.nfrag > G::FB) {  // a pixel deeper than FB can only exist if nfrag > FB
+    if (kp.f.nfrag > G::FBW) {  // a pixel deeper than FBW can only exist if nfrag > FBW
         long_pixel_kernel<R><<<64, kLongT, ls, st>>>(kp);
         err = cudaGetLastError();
     }

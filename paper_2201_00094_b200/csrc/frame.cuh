@@ -32,61 +32,68 @@ struct KParams {
     int64_t long_cap;
 };
 
-// per-rank tile geometry
+// per-rank warp-tile geometry
 template <int R>
-struct RT {
+struct WT {
     static constexpr int S = 1 << (R + 1);   // coefficient slots (== cells M)
     static constexpr int V = 3 * S;          // values per pixel
-    static constexpr int T = R <= 4 ? 128 : (R == 5 ? 64 : 32);  // threads = chunk slots
-    static constexpr int CH = 16;            // fragments per chunk (max)
-    static constexpr int FB = T * CH;        // fragments per sub-tile (max)
-    static constexpr int PB_RAW = 24576 / (V * 8);
-    static constexpr int PB = PB_RAW < T ? PB_RAW : T;  // pixels per CTA window
-    static constexpr int VP = V + 1;         // padded coef64 row
+    static constexpr int CH = 8;             // fragments per chunk (max)
+    static constexpr int FBW = 32 * CH;      // fragments per warp sub-tile (max)
+    static constexpr int WIN = 32;           // pixels per warp window
+    static constexpr int SUBP = 10;          // pixels per sub-tile (3 SUBP <= 32 (pixel, channel) tasks)
+    static constexpr int WPB = R <= 3 ? 2 : 1;  // warps per CTA
 };
 
-struct Layout {
-    uint32_t offs, nch, cb, nearu, faru, lo, den, vtot, chunk;
-    uint32_t depth, alpha, trans, rad, ior, normal, bf, zfix, r1, r2, bar, total;
+struct WLayout {
+    uint32_t offs, nch, cb, rot, nearu, faru, lo, den, rcp, vtot, chunk;
+    uint32_t depth, alpha, trans, rad, ior, normal, bf, zfix, part, cells, coef32, accp, pk, bar, total;
 };
 
 WOIT_HD uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
 
+// shared-memory slice of one warp (bytes); the CTA holds WPB slices
 template <int R>
-WOIT_HD Layout make_layout(uint32_t phases, int flags) {
-    using G = RT<R>;
-    const bool frag = phases & (PH_BOUNDS | PH_BUILD | PH_EVAL);
+WOIT_HD WLayout make_wlayout(uint32_t phases, int flags) {
+    using G = WT<R>;
     const bool at = phases & (PH_BUILD | PH_EVAL);
     const bool ev = phases & PH_EVAL;
     const bool need_ior = at && (flags & (WOIT_CUBE_TRANSMISSION | WOIT_REFRACTION));
     const bool need_bf = at && (flags & WOIT_CUBE_TRANSMISSION) && (flags & WOIT_CUBE_BACKFACE_ONLY);
     const bool need_nrm = ev && (flags & WOIT_REFRACTION);
-    const uint32_t FS = G::FB + 4;  // staging window: [fa & ~3, fb)
-    Layout L;
+    const bool packed = (phases & PH_BUILD) && (flags & WOIT_PACKED_STORAGE);
+    const uint32_t FS = G::FBW + 4;  // staging window: [fa & ~3, fb)
+    WLayout L;
     uint32_t o = 0;
-    L.offs = o;  o = align16(o + 8u * (G::PB + 1));
-    L.nch = o;   o = align16(o + 8u * G::PB);
-    L.cb = o;    o = align16(o + 8u * (G::T + 1));
-    L.nearu = o; o = align16(o + 4u * G::PB);
-    L.faru = o;  o = align16(o + 4u * G::PB);
-    L.lo = o;    o = align16(o + 8u * G::PB);
-    L.den = o;   o = align16(o + 8u * G::PB);
-    L.vtot = o;  o = align16(o + 8u * 3 * G::PB);
-    L.chunk = o; o = align16(o + 4u * G::T);
-    L.depth = o; o = align16(o + (frag ? 4u * FS : 0u));
+    L.offs = o;  o = align16(o + 8u * (G::WIN + 1));
+    L.nch = o;   o = align16(o + 4u * G::WIN);
+    L.cb = o;    o = align16(o + 4u * (G::WIN + 1));
+    L.rot = o;   o = align16(o + 4u * G::WIN);
+    L.nearu = o; o = align16(o + 4u * G::WIN);
+    L.faru = o;  o = align16(o + 4u * G::WIN);
+    L.lo = o;    o = align16(o + 8u * G::WIN);
+    L.den = o;   o = align16(o + 8u * G::WIN);
+    L.rcp = o;   o = align16(o + 8u * G::WIN);
+    L.vtot = o;  o = align16(o + 8u * 3 * G::WIN);
+    L.chunk = o; o = align16(o + 4u * 32);
+    L.depth = o; o = align16(o + 4u * FS);
     L.alpha = o; o = align16(o + (at ? 4u * FS : 0u));
     L.trans = o; o = align16(o + (at ? 12u * FS : 0u));
     L.rad = o;   o = align16(o + (ev ? 12u * FS : 0u));
     L.ior = o;   o = align16(o + (need_ior ? 4u * FS : 0u));
     L.normal = o; o = align16(o + (need_nrm ? 12u * FS : 0u));
-    L.bf = o;    o = align16(o + (need_bf ? (uint32_t)G::FB + 32u : 0u));
-    L.zfix = o;  o = align16(o + ((phases & PH_BUILD) && ev ? 8u * G::FB : 0u));
-    const uint32_t r1a = 4u * G::V * G::T, r1b = 4u * G::PB * G::V;
-    L.r1 = o;    o = align16(o + (r1a > r1b ? r1a : r1b));
-    const uint32_t r2a = 8u * G::PB * G::VP, r2b = 4u * 8u * G::T;
-    L.r2 = o;    o = align16(o + (r2a > r2b ? r2a : r2b));
+    L.bf = o;    o = align16(o + (need_bf ? (uint32_t)G::FBW + 32u : 0u));
+    L.zfix = o;  o = align16(o + (at ? 8u * G::FBW : 0u));
+    // one region, reused: chunk partials [V][32] during the build, then the sub-tile's
+    // coefficients [SUBP][V], cell staircase [SUBP][V] and chunk accumulators [8][32]
+    const uint32_t part_b = (phases & PH_BUILD) ? 4u * G::V * 32 : 0u;
+    const uint32_t after_b = 2u * 4u * G::SUBP * G::V + (ev ? 4u * 8 * 32 : 0u);
+    L.part = o;  o = align16(o + (part_b > after_b ? part_b : after_b));
+    L.coef32 = L.part;
+    L.cells = L.part + 4u * G::SUBP * G::V;
+    L.accp = L.cells + 4u * G::SUBP * G::V;
+    L.pk = o;    o = align16(o + (packed ? 8u * G::WIN * G::V : 0u));
     L.bar = o;   o = align16(o + 16u);
-    L.total = o;
+    L.total = (o + 127u) & ~127u;
     return L;
 }
 
@@ -183,6 +190,21 @@ WOIT_D void composite_pixel(const KParams& kp, int64_t p, const double acc[3],
     } else {
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) out[ch] = (float)dadd(acc[ch], dmul(bg[ch], vtot[ch]));
+    }
+}
+
+// composite without refraction or aberration: background = the pixel's opaque colour
+WOIT_D void composite_plain(int flags, const float bgc[3], const double acc[3], const double wgt[3],
+                            const double vtot[3], float out[3]) {
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        const double bg = (double)bgc[ch];
+        if (flags & WOIT_NORMALIZE) {
+            const double avg = ddiv(acc[ch], fmax(kNormEps, wgt[ch]));
+            out[ch] = (float)dadd(dmul(avg, 1.0 - vtot[ch]), dmul(bg, vtot[ch]));
+        } else {
+            out[ch] = (float)dadd(acc[ch], dmul(bg, vtot[ch]));
+        }
     }
 }
 

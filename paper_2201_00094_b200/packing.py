@@ -53,7 +53,7 @@ def unpack_rgb9e5(words):
     lib = _lib.load()
     host = not isinstance(words, torch.Tensor)
     if host:
-        w = np.ascontiguousarray(np.asarray(words, dtype=np.uint32)).view(np.int32)
+        w = np.array(words, dtype=np.uint32, order="C", copy=True).view(np.int32)
         wt = torch.from_numpy(w).cuda()
     else:
         wt = words.to(torch.int32)

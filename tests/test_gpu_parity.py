@@ -188,8 +188,8 @@ def test_step1_accumulates_with_existing_bounds(W):
     bufs.far.fill_(1.6)
     W.step1_depth_bounds(frame, bufs)
     ref = O.OBuffers.allocate(O.OFrame.from_synth(sf), 3)
-    ref.near[:] = 1.5
-    ref.far[:] = 1.6
+    ref.near[:] = np.float32(1.5)
+    ref.far[:] = np.float32(1.6)
     O.step1_depth_bounds(O.OFrame.from_synth(sf), ref)
     np.testing.assert_array_equal(h(bufs.near), ref.near)
     np.testing.assert_array_equal(h(bufs.far), ref.far)

@@ -127,7 +127,7 @@ struct WSmem {
     float* ior;
     float* normal;
     uint8_t* bf;
-    int64_t* zfix;     // [FBW] z in fixed point, by fragment
+    zfix_t* zfix;      // [FBW] z in fixed point, by fragment
     float* part;       // [V][32] chunk partials (f64 [WIN][V] scratch for packed storage)
     float* cells;      // [WIN][V] staircase at cell centres
     float* coef32;     // [WIN][V] coefficients, bulk-stored to bufs->coeffs
@@ -157,7 +157,7 @@ WOIT_D WSmem<R, GEN> wcarve(unsigned char* base, const WLayout& L) {
     s.ior = reinterpret_cast<float*>(base + L.ior);
     s.normal = reinterpret_cast<float*>(base + L.normal);
     s.bf = reinterpret_cast<uint8_t*>(base + L.bf);
-    s.zfix = reinterpret_cast<int64_t*>(base + L.zfix);
+    s.zfix = reinterpret_cast<zfix_t*>(base + L.zfix);
     s.part = reinterpret_cast<float*>(base + L.part);
     s.cells = reinterpret_cast<float*>(base + L.cells);
     s.coef32 = reinterpret_cast<float*>(base + L.coef32);
@@ -358,19 +358,19 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
                 for (int v = 6; v < V; ++v) part[v * WC + lane] = 0.0f;
                 float s0[3] = {0.f, 0.f, 0.f}, s1[3] = {0.f, 0.f, 0.f};
                 int jj = crot;
-#pragma unroll 1
+#pragma unroll 2
                 for (int j = 0; j < clen; ++j) {
                     const int fr = cst + jj;   // fragment index relative to fa
                     jj = jj + 1 == clen ? 0 : jj + 1;
                     const int si = sh4 + fr;   // staging index
-                    const int64_t zi = sm.zfix[fr];
+                    const zfix_t zi = sm.zfix[fr];
                     const float al = sm.alpha[si];
                     bool cb_ = false;
                     if (cube) cb_ = sm.ior[si] > 1.0f && (!bfonly || sm.bf[shb + fr] != 0);
                     float a[3];
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) a[ch] = absorbance_ch(al, sm.trans[3 * si + ch], cb_);
-                    const float one_m_z = fixed_to_unit((int64_t(1) << kZBits) - zi, kZBits);
+                    const float one_m_z = one_minus_z(zi);
                     const float psi0 = level_psi(zi, 0);
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) {
@@ -523,7 +523,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
                     topq = kp.f.opaque_depth ? (double)kp.f.opaque_depth[p] : INFINITY;
                 }
                 int jj = crot;
-#pragma unroll 1
+#pragma unroll 2
                 for (int j = 0; j < clen; ++j) {
                     const int fr = cst + jj;
                     jj = jj + 1 == clen ? 0 : jj + 1;
@@ -573,8 +573,12 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
                     bulk_s2g(kp.b.vhat + 3 * i0, sm.rad + 3 * (i0 - a4), (uint32_t)(12 * (i1 - i0)));
                     bulk_commit();
                 }
-                for (int64_t f = fa + lane; f < fb; f += 32) {
-                    if (bulk && f >= i0 && f < i1) continue;
+                // lanes cover the ragged head [fa, i0) and tail [i1, fb) (< 4 each), or
+                // everything without TMA
+                const int nhead = bulk ? (int)(i0 - fa) : (int)(fb - fa);
+                const int ntail = bulk ? (int)(fb - i1) : 0;
+                for (int i = lane; i < nhead + ntail; i += 32) {
+                    const int64_t f = i < nhead ? fa + i : i1 + (i - nhead);
                     const int si = (int)(f - a4);
                     kp.b.vhat[3 * f] = sm.rad[3 * si];
                     kp.b.vhat[3 * f + 1] = sm.rad[3 * si + 1];
@@ -707,7 +711,7 @@ __global__ void __launch_bounds__(kLongT) long_pixel_kernel(const KParams kp) {
                 for (int v = 0; v < V; ++v) acc64[v * TL + tid] = 0.0;
                 for (int64_t f = s + tid; f < e; f += TL) {
                     const double z = normalized_z(kp.f.depth[f], m);
-                    const int64_t zi = z_fixed(z);
+                    const zfix_t zi = z_fixed(z);
                     const float al = kp.f.alpha[f];
                     bool cb_ = false;
                     if (cube) {
@@ -716,7 +720,7 @@ __global__ void __launch_bounds__(kLongT) long_pixel_kernel(const KParams kp) {
                     }
                     float a[3];
                     for (int ch = 0; ch < 3; ++ch) a[ch] = absorbance_ch(al, kp.f.trans[3 * f + ch], cb_);
-                    const float one_m_z = fixed_to_unit((int64_t(1) << kZBits) - zi, kZBits);
+                    const float one_m_z = one_minus_z(zi);
                     const float psi0 = level_psi(zi, 0);
                     for (int ch = 0; ch < 3; ++ch) {
                         acc64[ch * TL + tid] += (double)(a[ch] * one_m_z);
@@ -777,7 +781,7 @@ __global__ void __launch_bounds__(kLongT) long_pixel_kernel(const KParams kp) {
                 topq = kp.f.opaque_depth ? (double)kp.f.opaque_depth[p] : INFINITY;
             }
             for (int64_t f = s + tid; f < e; f += kLongT) {
-                const int64_t zi = z_fixed(normalized_z(kp.f.depth[f], m));
+                const zfix_t zi = z_fixed(normalized_z(kp.f.depth[f], m));
                 int c0, c1;
                 float t;
                 eval_cells(zi, R, c0, c1, t);
@@ -925,7 +929,7 @@ __global__ void indices_kernel(const KParams kp, double* z_out, int32_t* k_out, 
         const DepthMap m = depth_map(kp.b.near[p], kp.b.far[p], rank);
         for (int64_t f = kp.f.offsets[p]; f < kp.f.offsets[p + 1]; ++f) {
             const double z = normalized_z(kp.f.depth[f], m);
-            const int64_t zi = z_fixed(z);
+            const zfix_t zi = z_fixed(z);
             z_out[f] = z;
             for (int n = 0; n <= rank; ++n) k_out[f * (rank + 1) + n] = slot_offset(zi, n);
             int c0, c1;

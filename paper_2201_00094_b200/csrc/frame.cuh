@@ -82,7 +82,7 @@ WOIT_HD WLayout make_wlayout(uint32_t phases, int flags) {
     L.ior = o;   o = align16(o + (need_ior ? 4u * FS : 0u));
     L.normal = o; o = align16(o + (need_nrm ? 12u * FS : 0u));
     L.bf = o;    o = align16(o + (need_bf ? (uint32_t)G::FBW + 32u : 0u));
-    L.zfix = o;  o = align16(o + (at ? 8u * G::FBW : 0u));
+    L.zfix = o;  o = align16(o + (at ? 4u * G::FBW : 0u));
     // one region, reused: chunk partials [V][32] during the build, then the sub-tile's
     // coefficients [SUBP][V], cell staircase [SUBP][V] and chunk accumulators [8][32]
     const uint32_t part_b = (phases & PH_BUILD) ? 4u * G::V * 32 : 0u;

@@ -246,6 +246,12 @@ def run_ours(args, cfg):
         e2e = run_e2e(args, W, frame, rcfg, dev, world, pg)
 
     peak, peak_kind = peaks()
+    if args.traffic is None:
+        try:
+            with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
+                args.traffic = json.load(f).get(f"config{args.config}")
+        except Exception:
+            args.traffic = None
     alg = algorithmic_bytes(P, n, cfg["rank"])
     achieved = alg / (kern_ms * 1e-3) / 1e9
     clocks = clk.summary()

@@ -27,11 +27,11 @@ WOIT_D void unpack_chunk(uint32_t c, int& q, int& start, int& len) {
 // fragment id of the chunk start: it spreads the lanes of a warp over the 32
 // smem banks for uniform run lengths and keeps the summation order independent
 // of the tiling (bit-identical results for any band split).
-WOIT_D int chunk_rotation(int64_t gstart, int len) { return (int)((uint64_t)(gstart >> 5) % (uint64_t)len); }
+WOIT_D int chunk_rotation(int64_t gstart, int len) { return (int)((uint32_t)(gstart >> 5) % (uint32_t)len); }
 
 // rotation of the chunk loop in the per-pixel combine (same purpose)
 WOIT_D int combine_rotation(int64_t gpix, int nch) {
-    return (int)((uint64_t)((gpix * nch) >> 5) % (uint64_t)nch);
+    return (int)((uint32_t)((gpix * nch) >> 5) % (uint32_t)nch);
 }
 
 // ---------------------------------------------------------------------------
@@ -243,34 +243,57 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
         const int shb = (int)(fa - a16);
 
         // ---- 1. stage fragment fields (TMA bulk copies, one mbarrier per warp) ----
+        // All 4-byte-element and 12-byte-element arrays share the 16-B granule
+        // window [a4, b4): one bulk copy each; lanes load the < 4-fragment tail
+        // that ends the arrays (or everything without TMA). Backface bytes have a
+        // 16-fragment granule and their own window.
         {
-            StageSpec specs[7];
-            int nspec = 0;
-            specs[nspec++] = {kp.f.depth, sm.depth, 4, 4};
-            if (do_at) specs[nspec++] = {kp.f.alpha, sm.alpha, 4, 4};
-            if (do_at) specs[nspec++] = {kp.f.trans, sm.trans, 12, 4};
-            if (do_eval) specs[nspec++] = {kp.f.radiance, sm.rad, 12, 4};
-            if (GEN && need_ior && kp.f.ior) specs[nspec++] = {kp.f.ior, sm.ior, 4, 4};
-            if (GEN && refr) specs[nspec++] = {kp.f.normal, sm.normal, 12, 4};
-            if (GEN && bfonly && kp.f.backface) specs[nspec++] = {kp.f.backface, sm.bf, 1, 16};
+            const bool w_ior = GEN && need_ior && kp.f.ior;
+            const bool w_nrm = GEN && refr;
+            const bool w_bf = GEN && bfonly && kp.f.backface;
+            int64_t b4 = (fb + 3) & ~(int64_t)3;
+            b4 = b4 < (nalloc & ~(int64_t)3) ? b4 : (nalloc & ~(int64_t)3);
+            if (!kp.use_tma || b4 < a4) b4 = a4;
+            int64_t b16 = (fb + 15) & ~(int64_t)15;
+            b16 = b16 < (nalloc & ~(int64_t)15) ? b16 : (nalloc & ~(int64_t)15);
+            if (!kp.use_tma || b16 < a16) b16 = a16;
             if (kp.use_tma && lane == 0) {
                 bulk_wait_read_all();  // the previous sub-tile's stores have left smem
-                uint32_t tx = 0;
-                for (int i = 0; i < nspec; ++i) {
-                    int64_t a;
-                    const int64_t e = stage_bulk_end(specs[i], fa, fb, nalloc, 1, a);
-                    if (e > a) tx += (uint32_t)((e - a) * specs[i].esize);
-                }
+                const uint32_t n4 = (uint32_t)(b4 - a4);
+                const uint32_t per = 4u + (do_at ? 16u : 0u) + (do_eval ? 12u : 0u) + (w_ior ? 4u : 0u) +
+                                     (w_nrm ? 12u : 0u);
+                const uint32_t tx = n4 * per + (w_bf ? (uint32_t)(b16 - a16) : 0u);
                 mbar_arrive_expect_tx(sm.bar, tx);
-                for (int i = 0; i < nspec; ++i) {
-                    int64_t a;
-                    const int64_t e = stage_bulk_end(specs[i], fa, fb, nalloc, 1, a);
-                    if (e > a)
-                        bulk_g2s(specs[i].s, static_cast<const unsigned char*>(specs[i].g) + a * specs[i].esize,
-                                 (uint32_t)((e - a) * specs[i].esize), sm.bar);
+                if (n4) {
+                    bulk_g2s(sm.depth, kp.f.depth + a4, 4u * n4, sm.bar);
+                    if (do_at) {
+                        bulk_g2s(sm.alpha, kp.f.alpha + a4, 4u * n4, sm.bar);
+                        bulk_g2s(sm.trans, kp.f.trans + 3 * a4, 12u * n4, sm.bar);
+                    }
+                    if (do_eval) bulk_g2s(sm.rad, kp.f.radiance + 3 * a4, 12u * n4, sm.bar);
+                    if (w_ior) bulk_g2s(sm.ior, kp.f.ior + a4, 4u * n4, sm.bar);
+                    if (w_nrm) bulk_g2s(sm.normal, kp.f.normal + 3 * a4, 12u * n4, sm.bar);
                 }
+                if (w_bf && b16 > a16) bulk_g2s(sm.bf, kp.f.backface + a16, (uint32_t)(b16 - a16), sm.bar);
             }
-            for (int i = 0; i < nspec; ++i) stage_scalar<32>(specs[i], fa, fb, nalloc, kp.use_tma, lane);
+            for (int64_t i = (b4 > fa ? b4 : fa) + lane; i < fb; i += 32) {
+                const int si = (int)(i - a4);
+                sm.depth[si] = kp.f.depth[i];
+                if (do_at) {
+                    sm.alpha[si] = kp.f.alpha[i];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) sm.trans[3 * si + c] = kp.f.trans[3 * i + c];
+                }
+                if (do_eval)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) sm.rad[3 * si + c] = kp.f.radiance[3 * i + c];
+                if (w_ior) sm.ior[si] = kp.f.ior[i];
+                if (w_nrm)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) sm.normal[3 * si + c] = kp.f.normal[3 * i + c];
+            }
+            if (w_bf)
+                for (int64_t i = (b16 > fa ? b16 : fa) + lane; i < fb; i += 32) sm.bf[(int)(i - a16)] = kp.f.backface[i];
             if (GEN && need_ior && !kp.f.ior)
                 for (int i = lane; i < (int)(fb - fa); i += 32) sm.ior[sh4 + i] = 1.0f;
             if (GEN && bfonly && !kp.f.backface)
@@ -430,7 +453,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
                     double at = c[0];
 #pragma unroll
                     for (int n = 0; n <= R; ++n) at = dsub(at, dmul(kSqrt2Pow[n], c[(2 << n) - 1]));
-                    sm.vtot[kq * 3 + kch] = exp(-fmax(at, 0.0));
+                    sm.vtot[kq * 3 + kch] = (double)expf(-(float)fmax(at, 0.0));
                 }
                 if (do_eval) {
                     double cell[S];
@@ -468,7 +491,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
                         double at = c[0];
 #pragma unroll
                         for (int n = 0; n <= R; ++n) at = dsub(at, dmul(kSqrt2Pow[n], c[(2 << n) - 1]));
-                        sm.vtot[kq * 3 + kch] = exp(-fmax(at, 0.0));
+                        sm.vtot[kq * 3 + kch] = (double)expf(-(float)fmax(at, 0.0));
                     }
                     if (do_eval) {
                         double cell[S];
@@ -488,7 +511,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
                 double at = c[0];
 #pragma unroll
                 for (int n = 0; n <= R; ++n) at = dsub(at, dmul(kSqrt2Pow[n], c[(2 << n) - 1]));
-                sm.vtot[kq * 3 + kch] = exp(-fmax(at, 0.0));
+                sm.vtot[kq * 3 + kch] = (double)expf(-(float)fmax(at, 0.0));
                 double cell[S];
                 haar_cells<R>(c, cell);
 #pragma unroll

@@ -200,7 +200,7 @@ WOIT_D void composite_plain(int flags, const float bgc[3], const double acc[3], 
     for (int ch = 0; ch < 3; ++ch) {
         const double bg = (double)bgc[ch];
         if (flags & WOIT_NORMALIZE) {
-            const double avg = ddiv(acc[ch], fmax(kNormEps, wgt[ch]));
+            const double avg = acc[ch] * rcp_refined(fmax(kNormEps, wgt[ch]));
             out[ch] = (float)dadd(dmul(avg, 1.0 - vtot[ch]), dmul(bg, vtot[ch]));
         } else {
             out[ch] = (float)dadd(acc[ch], dmul(bg, vtot[ch]));

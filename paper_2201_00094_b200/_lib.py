@@ -11,7 +11,8 @@ import os
 from typing import Optional
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libwoit.so")
+# WOIT_LIB selects an alternative build (tuning variants, tools/variants.py)
+LIB_PATH = os.environ.get("WOIT_LIB") or os.path.join(_HERE, "libwoit.so")
 
 ABI_VERSION = 1
 

@@ -42,16 +42,20 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = LIB) -> str:
+    """Compile and link. ``defines`` (e.g. ("WOIT_UNROLL=4",)) build a tuning variant into
+    its own object directory and ``out`` library."""
+    build_dir = BUILD if not defines else os.path.join(BUILD, "v_" + "_".join(d.replace("=", "") for d in defines))
+    os.makedirs(build_dir, exist_ok=True)
+    dflags = ["-D" + d for d in defines]
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(REPO, "include", "woit.h")]
     objs, jobs = [], []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        o = os.path.join(build_dir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
-            jobs.append([nvcc(), *ARCH, *FLAGS, "-c", s, "-o", o])
+            jobs.append([nvcc(), *ARCH, *FLAGS, *dflags, "-c", s, "-o", o])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -65,17 +69,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 sys.stderr.write(r.stdout + r.stderr)
                 raise RuntimeError(f"nvcc failed: {' '.join(cmd)}")
     if logs:
-        with open(os.path.join(BUILD, "ptxas.log"), "w") as f:
+        with open(os.path.join(build_dir, "ptxas.log"), "w") as f:
             f.write("\n".join(logs))
-    if force or jobs or _stale(LIB, objs):
-        cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static"]
+    if force or jobs or _stale(out, objs):
+        cmd = [nvcc(), *ARCH, "-shared", "-o", out, *objs, "-cudart", "static"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("link of libwoit.so failed")
     if verbose:
-        print(LIB)
-    return LIB
+        print(out)
+    return out
 
 
 if __name__ == "__main__":

@@ -48,7 +48,8 @@ int run_frame(const woit_frags_t* f, const woit_params_t* p, woit_bufs_t* b, uin
     kp.p = *p;
     kp.b = *b;
     kp.phases = phases;
-    const void* ptrs[] = {f->depth, f->alpha, f->trans, f->radiance, f->normal, f->ior, f->backface, b->vhat};
+    const void* ptrs[] = {f->depth, f->alpha, f->trans, f->radiance, f->normal, f->ior, f->backface, b->vhat,
+                          f->opaque_color};
     bool al = true;
     for (const void* q : ptrs) al = al && (q == nullptr || aligned16(q));
     kp.use_tma = al ? 1 : 0;

@@ -11,6 +11,20 @@
 //   chunk partials in a fixed order in fp64 -> deterministic for any tiling.
 #include "frame.cuh"
 
+#ifndef WOIT_UNROLL
+#define WOIT_UNROLL 2
+#endif
+#ifndef WOIT_ZUNROLL
+#define WOIT_ZUNROLL 8
+#endif
+#ifndef WOIT_PERSIST  // resident CTAs per SM slot multiplier for the persistent grid (0: one CTA per 2 windows)
+#define WOIT_PERSIST 1
+#endif
+namespace woit {
+constexpr int kUnroll = WOIT_UNROLL;  // fragment-loop unroll (tuning knob)
+constexpr int kZUnroll = WOIT_ZUNROLL;  // z-loop unroll
+}
+
 namespace woit {
 
 // chunk descriptor: pixel (8 bits), start within sub-tile (13 bits), length (5 bits)
@@ -133,6 +147,7 @@ struct WSmem {
     float* coef32;     // [WIN][V] coefficients, bulk-stored to bufs->coeffs
     float* accp;       // [8][32] chunk accumulators
     double* pk;        // [WIN][V] f64 coefficients for packed storage
+    float* opq;        // [SUBP+4][3] staged opaque colours of the sub-tile (fast path)
     uint64_t* bar;
 };
 
@@ -163,14 +178,17 @@ WOIT_D WSmem<R, GEN> wcarve(unsigned char* base, const WLayout& L) {
     s.coef32 = reinterpret_cast<float*>(base + L.coef32);
     s.accp = reinterpret_cast<float*>(base + L.accp);
     s.pk = reinterpret_cast<double*>(base + L.pk);
+    s.opq = reinterpret_cast<float*>(base + L.opq);
     s.bar = reinterpret_cast<uint64_t*>(base + L.bar);
     return s;
 }
 
 template <int R, bool GEN>
-__global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp) {
+__global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel(const KParams kp) {
     using G = WT<R>;
     constexpr int S = G::S, V = G::V, CH = G::CH, WC = 32, FBW = G::FBW, WIN = G::WIN, SUBP = G::SUBP;
+    constexpr int VR = G::VR;  // padded row of the cell table: (pixel, channel) lanes hit distinct banks
+    constexpr int M = S;       // cells
     constexpr uint32_t kFused = PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const uint32_t ph = GEN ? kp.phases : kFused;
@@ -179,9 +197,12 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
     const int lane = threadIdx.x & 31;
     WSmem<R, GEN> sm = wcarve<R, GEN>(smem_raw + (threadIdx.x >> 5) * L.total, L);
 
-    const int64_t w0 = ((int64_t)blockIdx.x * G::WPB + (threadIdx.x >> 5)) * WIN;
-    if (w0 >= kp.f.npix) return;  // warp-uniform
-    const int nq = (int)((kp.f.npix - w0) < WIN ? (kp.f.npix - w0) : WIN);
+    // persistent warps: window w = warp id + k * (total warps), next window's CSR
+    // offsets prefetched into registers while the current one is processed
+    const int64_t nwin = (kp.f.npix + WIN - 1) / WIN;
+    const int64_t wstride = (int64_t)gridDim.x * G::WPB;
+    int64_t win = (int64_t)blockIdx.x * G::WPB + (threadIdx.x >> 5);
+    if (win >= nwin) return;  // warp-uniform
 
     const bool do_at = ph & (PH_BUILD | PH_EVAL);
     const bool do_eval = ph & PH_EVAL;
@@ -194,8 +215,27 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
     const int64_t nalloc = kp.f.nfrag;
 
     if (lane == 0) mbar_init(sm.bar, 1);
-    if (lane <= nq) sm.offs[lane] = kp.f.offsets[w0 + lane];
-    if (lane == 0 && nq == 32) sm.offs[32] = kp.f.offsets[w0 + 32];
+    uint32_t parity = 0;
+    int64_t off_lane = 0, off_last;  // this window's offsets[lane] and offsets[end]
+    {
+        const int64_t end = (win * WIN + WIN) < kp.f.npix ? (win * WIN + WIN) : kp.f.npix;
+        if (win * WIN + lane < end) off_lane = kp.f.offsets[win * WIN + lane];
+        off_last = kp.f.offsets[end];
+    }
+    for (; win < nwin; win += wstride) {
+    const int64_t w0 = win * WIN;
+    const int nq = (int)((kp.f.npix - w0) < WIN ? (kp.f.npix - w0) : WIN);
+    if (lane < nq) sm.offs[lane] = off_lane;
+    if (lane == 0) sm.offs[nq] = off_last;
+    {   // prefetch the next window's offsets (consumed one window later)
+        const int64_t nw = win + wstride;
+        if (nw < nwin) {
+            const int64_t nw0 = nw * WIN;
+            const int64_t nend = (nw0 + WIN) < kp.f.npix ? (nw0 + WIN) : kp.f.npix;
+            if (nw0 + lane < nend) off_lane = kp.f.offsets[nw0 + lane];
+            off_last = kp.f.offsets[nend];
+        }
+    }
     __syncwarp();
     // chunks per pixel, window prefix (warp scan) and combine rotation
     int my_nch = 0;
@@ -216,7 +256,6 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
     if (lane == 0) sm.cb[0] = 0;
     __syncwarp();
 
-    uint32_t parity = 0;
     int q0 = 0;
     while (q0 < nq) {
         // sub-tile end: largest q1 with <= FBW fragments and <= 32 chunks
@@ -257,12 +296,18 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
             int64_t b16 = (fb + 15) & ~(int64_t)15;
             b16 = b16 < (nalloc & ~(int64_t)15) ? b16 : (nalloc & ~(int64_t)15);
             if (!kp.use_tma || b16 < a16) b16 = a16;
+            // fast path: the sub-tile's opaque colours ride along (12 B/pixel, 4-pixel granule)
+            const int64_t pa = w0 + q0, pb = w0 + q1, pa4 = pa & ~(int64_t)3;
+            int64_t pb4 = (pb + 3) & ~(int64_t)3;
+            pb4 = pb4 < (kp.f.npix & ~(int64_t)3) ? pb4 : (kp.f.npix & ~(int64_t)3);
+            if (GEN || !kp.use_tma || pb4 < pa4) pb4 = pa4;
             if (kp.use_tma && lane == 0) {
                 bulk_wait_read_all();  // the previous sub-tile's stores have left smem
                 const uint32_t n4 = (uint32_t)(b4 - a4);
                 const uint32_t per = 4u + (do_at ? 16u : 0u) + (do_eval ? 12u : 0u) + (w_ior ? 4u : 0u) +
                                      (w_nrm ? 12u : 0u);
-                const uint32_t tx = n4 * per + (w_bf ? (uint32_t)(b16 - a16) : 0u);
+                const uint32_t tx = n4 * per + (w_bf ? (uint32_t)(b16 - a16) : 0u) + 12u * (uint32_t)(pb4 - pa4);
+                if (pb4 > pa4) bulk_g2s(sm.opq, kp.f.opaque_color + 3 * pa4, 12u * (uint32_t)(pb4 - pa4), sm.bar);
                 mbar_arrive_expect_tx(sm.bar, tx);
                 if (n4) {
                     bulk_g2s(sm.depth, kp.f.depth + a4, 4u * n4, sm.bar);
@@ -292,6 +337,13 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
 #pragma unroll
                     for (int c = 0; c < 3; ++c) sm.normal[3 * si + c] = kp.f.normal[3 * i + c];
             }
+            if (!GEN)
+                for (int64_t p = (pb4 > pa ? pb4 : pa) + lane; p < pb; p += 32) {
+                    const int si = (int)(p - pa4);
+                    sm.opq[3 * si] = kp.f.opaque_color[3 * p];
+                    sm.opq[3 * si + 1] = kp.f.opaque_color[3 * p + 1];
+                    sm.opq[3 * si + 2] = kp.f.opaque_color[3 * p + 2];
+                }
             if (w_bf)
                 for (int64_t i = (b16 > fa ? b16 : fa) + lane; i < fb; i += 32) sm.bf[(int)(i - a16)] = kp.f.backface[i];
             if (GEN && need_ior && !kp.f.ior)
@@ -301,7 +353,6 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
         }
 
         // ---- 2. chunk table + per-pixel init (overlaps the copies) -----------------
-        float bgc[3] = {0.f, 0.f, 0.f};
         if (lane < nqs) {
             const int q = q0 + lane;
             const int run = (int)(sm.offs[q + 1] - sm.offs[q]);
@@ -318,11 +369,6 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
                 }
             }
             const int64_t p = w0 + q;
-            if (!GEN) {  // background of the composite, fetched early to hide its latency
-                bgc[0] = kp.f.opaque_color[p * 3];
-                bgc[1] = kp.f.opaque_color[p * 3 + 1];
-                bgc[2] = kp.f.opaque_color[p * 3 + 2];
-            }
             const bool init_empty = (ph & PH_BOUNDS) && !(ph & PH_BOUNDS_ACC);
             sm.nearu[lane] = f2ord(init_empty ? INFINITY : kp.b.near[p]);
             sm.faru[lane] = f2ord(init_empty ? -INFINITY : kp.b.far[p]);
@@ -344,8 +390,10 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
         if (ph & PH_BOUNDS) {
             if (lane < C) {
                 float mn = INFINITY, mx = -INFINITY;
+                int jj = crot;  // rotated start: conflict-free banks across lanes
                 for (int j = 0; j < clen; ++j) {
-                    const float x = sm.depth[sh4 + cst + j];
+                    const float x = sm.depth[sh4 + cst + jj];
+                    jj = jj + 1 == clen ? 0 : jj + 1;
                     mn = fminf(mn, x);
                     mx = fmaxf(mx, x);
                 }
@@ -370,18 +418,33 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
         float* part = sm.part;
         if (lane < C && do_at) {
             const DepthMap m{sm.lo[cq], sm.den[cq], sm.rcp[cq]};
-            for (int j = 0; j < clen; ++j) {
-                const int fr = cst + j;
-                sm.zfix[fr] = z_fixed(normalized_z(sm.depth[sh4 + fr], m));
+#pragma unroll kZUnroll
+            for (int j = 0; j < CH; ++j) {  // independent chains: unrolled for ILP
+                if (j < clen) {
+                    int jj = crot + j;
+                    jj = jj >= clen ? jj - clen : jj;
+                    const int fr = cst + jj;
+                    sm.zfix[fr] = z_fixed(normalized_z(sm.depth[sh4 + fr], m));
+                }
             }
         }
+        // The rank-N Haar space (scaling + levels 0..N, M = 2^(N+1) slots) is exactly
+        // the piecewise constants on M cells, so the projection of the absorbance
+        // staircase is its cell averages: v_c = sum_{j_f < c} a_f + sum_{j_f = c} a_f w_f
+        // with j_f = floor(M z_f) and w_f = (j_f + 1) - M z_f. In differences
+        // D_c = v_c - v_{c-1} a fragment adds a w to D_j and a (1 - w) to D_{j+1}:
+        // two updates per channel, all terms >= 0 (no cancellation), and v is the
+        // prefix sum of D. The reference's coefficients are the Haar analysis of v
+        // (phase 5) -- its closed form (wavelet.py:272-287) up to rounding.
         if (ph & PH_BUILD) {
+            {   // zero the partials [M][3][32] cooperatively, 16 B per store
+                float4* pz = reinterpret_cast<float4*>(part);
+                for (int i = lane; i < (M * 3 * WC) / 4; i += 32) pz[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            __syncwarp();
             if (lane < C) {
-#pragma unroll
-                for (int v = 6; v < V; ++v) part[v * WC + lane] = 0.0f;
-                float s0[3] = {0.f, 0.f, 0.f}, s1[3] = {0.f, 0.f, 0.f};
                 int jj = crot;
-#pragma unroll 2
+#pragma unroll kUnroll
                 for (int j = 0; j < clen; ++j) {
                     const int fr = cst + jj;   // fragment index relative to fa
                     jj = jj + 1 == clen ? 0 : jj + 1;
@@ -393,26 +456,14 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
                     float a[3];
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) a[ch] = absorbance_ch(al, sm.trans[3 * si + ch], cb_);
-                    const float one_m_z = one_minus_z(zi);
-                    const float psi0 = level_psi(zi, 0);
+                    const int cell = (int)(zi >> (kZBits - (R + 1)));
+                    const float fr_ = u32_to_unit(zi << (R + 1), kZBits);  // M z - j_f
+                    float* d = part + cell * 3 * WC + lane;
 #pragma unroll
-                    for (int ch = 0; ch < 3; ++ch) {
-                        s0[ch] += a[ch] * one_m_z;
-                        s1[ch] -= a[ch] * psi0;
-                    }
+                    for (int ch = 0; ch < 3; ++ch) d[ch * WC] += a[ch] * (1.0f - fr_);
+                    if (cell + 1 < M)
 #pragma unroll
-                    for (int n = 1; n <= R; ++n) {
-                        const int k = slot_offset(zi, n);
-                        const float psi = level_psi(zi, n) * kInvSqrt2PowF[n];
-                        float* col = part + ((1 << n) + k) * 3 * WC + lane;
-#pragma unroll
-                        for (int ch = 0; ch < 3; ++ch) col[ch * WC] -= a[ch] * psi;
-                    }
-                }
-#pragma unroll
-                for (int ch = 0; ch < 3; ++ch) {
-                    part[ch * WC + lane] = s0[ch];
-                    part[(3 + ch) * WC + lane] = s1[ch];
+                        for (int ch = 0; ch < 3; ++ch) d[(3 + ch) * WC] += a[ch] * fr_;
                 }
             }
             __syncwarp();
@@ -428,39 +479,59 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
             const bool task = t < nqs * 3;
             const int kch = task ? t / nqs : 0, kq = task ? t - kch * nqs : 0;
             double c[S];
+            float rc[M];
             if (task) {
                 const int q = q0 + kq;
                 const int nc = sm.nch[q];
                 const int cbq = sm.cb[q] - sm.cb[q0];
-                const int r = sm.rot[q];
+                int r = sm.rot[q] + kch;  // channel offset: the three channel groups hit distinct banks
+                r = r >= nc ? r % nc : r;
                 const float* pv = part + kch * WC + cbq;
 #pragma unroll
-                for (int s = 0; s < S; ++s)
-                    c[s] = (GEN && (ph & PH_BUILD_ACC)) ? (double)kp.b.coeffs[(w0 + q) * V + 3 * s + kch] : 0.0;
+                for (int k = 0; k < M; ++k) rc[k] = 0.0f;
                 int ii = r;
 #pragma unroll 1
                 for (int i = 0; i < nc; ++i) {
 #pragma unroll
-                    for (int s = 0; s < S; ++s) c[s] += (double)pv[s * 3 * WC + ii];
+                    for (int k = 0; k < M; ++k) rc[k] += pv[k * 3 * WC + ii];
                     ii = ii + 1 == nc ? 0 : ii + 1;
                 }
+                // cell averages v_c = D_0 + ... + D_c, all terms >= 0
+#pragma unroll
+                for (int k = 1; k < M; ++k) rc[k] += rc[k - 1];
             }
+            // every lane has read its partials: the region now takes coefficients and cells
             __syncwarp();
+            if (task) {
+                const int q = q0 + kq;
+                if (do_eval)
+#pragma unroll
+                    for (int k = 0; k < M; ++k) sm.cells[kq * VR + 3 * k + kch] = rc[k];
+                if (need_coef) sm.vtot[kq * 3 + kch] = (double)expf(-rc[M - 1]);  // A(z -> 1) = v_{M-1}
+                // coefficients: Haar analysis of v in f64 (wavelet.py:3-9 layout):
+                // c[2^n + k] = 2^(n/2)/M (sum left half - sum right half), c[0] = mean
+                double T[M];
+#pragma unroll
+                for (int k = 0; k < M; ++k) T[k] = (double)rc[k];
+#pragma unroll
+                for (int m = 0; m <= R; ++m) {
+                    const int half = M >> (m + 1);  // wavelets at level n = R - m
+#pragma unroll
+                    for (int k = 0; k < half; ++k) {
+                        const double x = T[2 * k], y = T[2 * k + 1];
+                        c[half + k] = dmul(dmul(dsub(x, y), kSqrt2Pow[R - m]), 1.0 / M);
+                        T[k] = dadd(x, y);
+                    }
+                }
+                c[0] = dmul(T[0], 1.0 / M);
+                if (GEN && (ph & PH_BUILD_ACC)) {
+#pragma unroll
+                    for (int s = 0; s < S; ++s) c[s] = dadd(c[s], (double)kp.b.coeffs[(w0 + q) * V + 3 * s + kch]);
+                }
+            }
             if (!packed && task) {
 #pragma unroll
                 for (int s = 0; s < S; ++s) sm.coef32[kq * V + 3 * s + kch] = (float)c[s];
-                if (need_coef) {
-                    double at = c[0];
-#pragma unroll
-                    for (int n = 0; n <= R; ++n) at = dsub(at, dmul(kSqrt2Pow[n], c[(2 << n) - 1]));
-                    sm.vtot[kq * 3 + kch] = (double)expf(-(float)fmax(at, 0.0));
-                }
-                if (do_eval) {
-                    double cell[S];
-                    haar_cells<R>(c, cell);
-#pragma unroll
-                    for (int s = 0; s < S; ++s) sm.cells[kq * V + 3 * s + kch] = (float)cell[s];
-                }
             }
             if (GEN && packed && task) {
                 // the shared exponent couples the channels: stage the f64 coefficients
@@ -497,7 +568,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
                         double cell[S];
                         haar_cells<R>(c, cell);
 #pragma unroll
-                        for (int s = 0; s < S; ++s) sm.cells[kq * V + 3 * s + kch] = (float)cell[s];
+                        for (int s = 0; s < S; ++s) sm.cells[kq * VR + 3 * s + kch] = (float)cell[s];
                     }
                 }
             }
@@ -515,7 +586,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
                 double cell[S];
                 haar_cells<R>(c, cell);
 #pragma unroll
-                for (int s = 0; s < S; ++s) sm.cells[kq * V + 3 * s + kch] = (float)cell[s];
+                for (int s = 0; s < S; ++s) sm.cells[kq * VR + 3 * s + kch] = (float)cell[s];
             }
         }
         fence_proxy_async();  // coef32 becomes visible to the bulk store
@@ -536,7 +607,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
         // ---- 6. evaluate (step3): v̂ per fragment, chunk accumulators --------------
         if (do_eval) {
             if (lane < C) {
-                const float* cqv = sm.cells + cq * V;
+                const float* cqv = sm.cells + cq * VR;
                 float ac[3] = {0.f, 0.f, 0.f}, wg[3] = {0.f, 0.f, 0.f};
                 double ro[2] = {0.0, 0.0};
                 double d[3] = {0.0, 0.0, 0.0}, topq = INFINITY;
@@ -546,7 +617,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
                     topq = kp.f.opaque_depth ? (double)kp.f.opaque_depth[p] : INFINITY;
                 }
                 int jj = crot;
-#pragma unroll 2
+#pragma unroll kUnroll
                 for (int j = 0; j < clen; ++j) {
                     const int fr = cst + jj;
                     jj = jj + 1 == clen ? 0 : jj + 1;
@@ -656,6 +727,8 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
                 if (GEN) {
                     composite_pixel(kp, p, acc, wgt, ro[0], ro[1], sm.vtot + 3 * lane, out);
                 } else {
+                    const int si = (int)(p - ((w0 + q0) & ~(int64_t)3));
+                    const float bgc[3] = {sm.opq[3 * si], sm.opq[3 * si + 1], sm.opq[3 * si + 2]};
                     composite_plain(flags, bgc, acc, wgt, sm.vtot + 3 * lane, out);
                 }
 #pragma unroll
@@ -666,6 +739,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32) frame_kernel(const KParams kp
         __syncwarp();
         q0 = q1;
     }
+    }  // window loop
     if (lane == 0) bulk_wait_all();
 }
 
@@ -882,8 +956,18 @@ cudaError_t launch_tiles(const KParams& kp, cudaStream_t st) {
     const int bytes = (int)(L.total * G::WPB);
     cudaError_t err = cudaFuncSetAttribute(frame_kernel<R, GEN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (err != cudaSuccess) return err;
+    // persistent grid: as many CTAs as can be resident, each warp loops over windows
     const int64_t warps = (kp.f.npix + G::WIN - 1) / G::WIN;
-    const int64_t grid = (warps + G::WPB - 1) / G::WPB;
+    int64_t grid = (warps + G::WPB - 1) / G::WPB;
+    int dev = 0, sms = 148, per_sm = 1;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frame_kernel<R, GEN>, G::WPB * 32, bytes) !=
+            cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    cudaGetLastError();
+    const int64_t resident = (int64_t)sms * per_sm * WOIT_PERSIST;
+    if (WOIT_PERSIST > 0) grid = grid < resident ? grid : resident;
     if (grid > 0) {
         frame_kernel<R, GEN><<<(unsigned)grid, G::WPB * 32, bytes, st>>>(kp);
         err = cudaGetLastError();

@@ -9,6 +9,10 @@
 #include "common.cuh"
 #include "packing.cuh"
 
+#ifndef WOIT_WPB
+#define WOIT_WPB 2
+#endif
+
 namespace woit {
 
 // which passes a launch performs (the step entry points use subsets)
@@ -41,12 +45,13 @@ struct WT {
     static constexpr int FBW = 32 * CH;      // fragments per warp sub-tile (max)
     static constexpr int WIN = 32;           // pixels per warp window
     static constexpr int SUBP = 10;          // pixels per sub-tile (3 SUBP <= 32 (pixel, channel) tasks)
-    static constexpr int WPB = R <= 3 ? 2 : 1;  // warps per CTA
+    static constexpr int WPB = R <= 3 ? WOIT_WPB : 1;  // warps per CTA
+    static constexpr int VR = V + ((35 - V % 32) % 32);  // row stride == 3 (mod 32), >= V
 };
 
 struct WLayout {
     uint32_t offs, nch, cb, rot, nearu, faru, lo, den, rcp, vtot, chunk;
-    uint32_t depth, alpha, trans, rad, ior, normal, bf, zfix, part, cells, coef32, accp, pk, bar, total;
+    uint32_t depth, alpha, trans, rad, ior, normal, bf, zfix, part, cells, coef32, accp, pk, opq, bar, total;
 };
 
 WOIT_HD uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
@@ -83,15 +88,17 @@ WOIT_HD WLayout make_wlayout(uint32_t phases, int flags) {
     L.normal = o; o = align16(o + (need_nrm ? 12u * FS : 0u));
     L.bf = o;    o = align16(o + (need_bf ? (uint32_t)G::FBW + 32u : 0u));
     L.zfix = o;  o = align16(o + (at ? 4u * G::FBW : 0u));
-    // one region, reused: chunk partials [V][32] during the build, then the sub-tile's
-    // coefficients [SUBP][V], cell staircase [SUBP][V] and chunk accumulators [8][32]
+    // one region, reused: chunk partials [M][3][32] (per-cell differences D) during the
+    // build, then the sub-tile's coefficients [SUBP][V], cell staircase [SUBP][VR]
+    // and chunk accumulators [8][32]
     const uint32_t part_b = (phases & PH_BUILD) ? 4u * G::V * 32 : 0u;
-    const uint32_t after_b = 2u * 4u * G::SUBP * G::V + (ev ? 4u * 8 * 32 : 0u);
+    const uint32_t after_b = 4u * G::SUBP * G::V + 4u * G::SUBP * G::VR + (ev ? 4u * 8 * 32 : 0u);
     L.part = o;  o = align16(o + (part_b > after_b ? part_b : after_b));
     L.coef32 = L.part;
-    L.cells = L.part + 4u * G::SUBP * G::V;
-    L.accp = L.cells + 4u * G::SUBP * G::V;
+    L.cells = L.part + align16(4u * G::SUBP * G::V);
+    L.accp = L.cells + align16(4u * G::SUBP * G::VR);
     L.pk = o;    o = align16(o + (packed ? 8u * G::WIN * G::V : 0u));
+    L.opq = o;   o = align16(o + 12u * (G::SUBP + 8));
     L.bar = o;   o = align16(o + 16u);
     L.total = (o + 127u) & ~127u;
     return L;

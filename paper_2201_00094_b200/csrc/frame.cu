@@ -112,6 +112,24 @@ WOIT_D void haar_cells(const double c[], double cell[]) {
     (void)S;
 }
 
+// cell table entry (v_c, v_{c+1} - v_c) for one (pixel, channel) of the sub-tile;
+// pixel rows of CR float2 (CR == 3 mod 16) put the (pixel, channel) lanes on
+// distinct banks
+template <int M>
+struct CellRow {
+    static constexpr int CR = 3 * M + ((3 - 3 * M) % 16 + 16) % 16;
+};
+
+template <int M, typename TV>
+WOIT_D void store_cells(float2* cells, int kq, int kch, const TV v[M]) {
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+        const float vc = (float)v[c];
+        const float dv = c + 1 < M ? (float)v[c + 1] - vc : 0.0f;
+        cells[kq * CellRow<M>::CR + c * 3 + kch] = make_float2(vc, dv);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // The fused frame kernel. Every warp owns a window of WIN consecutive pixels and
 // processes it in sub-tiles of <= 32 chunks (<= 256 fragments) on its own slice
@@ -143,7 +161,7 @@ struct WSmem {
     uint8_t* bf;
     zfix_t* zfix;      // [FBW] z in fixed point, by fragment
     float* part;       // [V][32] chunk partials (f64 [WIN][V] scratch for packed storage)
-    float* cells;      // [WIN][V] staircase at cell centres
+    float2* cells;     // [SUBP][M][3] (v_c, v_{c+1} - v_c): staircase at cell centres
     float* coef32;     // [WIN][V] coefficients, bulk-stored to bufs->coeffs
     float* accp;       // [8][32] chunk accumulators
     double* pk;        // [WIN][V] f64 coefficients for packed storage
@@ -174,7 +192,7 @@ WOIT_D WSmem<R, GEN> wcarve(unsigned char* base, const WLayout& L) {
     s.bf = reinterpret_cast<uint8_t*>(base + L.bf);
     s.zfix = reinterpret_cast<zfix_t*>(base + L.zfix);
     s.part = reinterpret_cast<float*>(base + L.part);
-    s.cells = reinterpret_cast<float*>(base + L.cells);
+    s.cells = reinterpret_cast<float2*>(base + L.cells);
     s.coef32 = reinterpret_cast<float*>(base + L.coef32);
     s.accp = reinterpret_cast<float*>(base + L.accp);
     s.pk = reinterpret_cast<double*>(base + L.pk);
@@ -244,7 +262,6 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
         const int64_t nc64 = (run + CH - 1) / CH;
         my_nch = nc64 > (1 << 24) ? (1 << 24) : (int)nc64;  // long pixels never form a sub-tile
         sm.nch[lane] = my_nch;
-        sm.rot[lane] = my_nch > 0 ? combine_rotation(kp.f.pixel_base + w0 + lane, my_nch) : 0;
     }
     int inc = my_nch;
 #pragma unroll
@@ -455,7 +472,11 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
                     if (cube) cb_ = sm.ior[si] > 1.0f && (!bfonly || sm.bf[shb + fr] != 0);
                     float a[3];
 #pragma unroll
-                    for (int ch = 0; ch < 3; ++ch) a[ch] = absorbance_ch(al, sm.trans[3 * si + ch], cb_);
+                    for (int ch = 0; ch < 3; ++ch) {
+                        const float op = opacity_ch(al, sm.trans[3 * si + ch], cb_);
+                        sm.trans[3 * si + ch] = op;  // the evaluation's weight 1 - t (pipeline.py:184)
+                        a[ch] = -log_poly(fmaxf((float)kTransFloor, 1.0f - op));
+                    }
                     const int cell = (int)(zi >> (kZBits - (R + 1)));
                     const float fr_ = u32_to_unit(zi << (R + 1), kZBits);  // M z - j_f
                     float* d = part + cell * 3 * WC + lane;
@@ -484,17 +505,29 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
                 const int q = q0 + kq;
                 const int nc = sm.nch[q];
                 const int cbq = sm.cb[q] - sm.cb[q0];
-                int r = sm.rot[q] + kch;  // channel offset: the three channel groups hit distinct banks
-                r = r >= nc ? r % nc : r;
                 const float* pv = part + kch * WC + cbq;
 #pragma unroll
                 for (int k = 0; k < M; ++k) rc[k] = 0.0f;
-                int ii = r;
+                // chunks summed in chunk order (fixed by the pixel's run length only);
+                // 16-B vector loads when the pixel's chunk group is 4-aligned
+                if (((cbq | nc) & 3) == 0) {
 #pragma unroll 1
-                for (int i = 0; i < nc; ++i) {
+                    for (int i = 0; i < nc; i += 4) {
 #pragma unroll
-                    for (int k = 0; k < M; ++k) rc[k] += pv[k * 3 * WC + ii];
-                    ii = ii + 1 == nc ? 0 : ii + 1;
+                        for (int k = 0; k < M; ++k) {
+                            const float4 p4 = *reinterpret_cast<const float4*>(pv + k * 3 * WC + i);
+                            rc[k] += p4.x;
+                            rc[k] += p4.y;
+                            rc[k] += p4.z;
+                            rc[k] += p4.w;
+                        }
+                    }
+                } else {
+#pragma unroll 1
+                    for (int i = 0; i < nc; ++i) {
+#pragma unroll
+                        for (int k = 0; k < M; ++k) rc[k] += pv[k * 3 * WC + i];
+                    }
                 }
                 // cell averages v_c = D_0 + ... + D_c, all terms >= 0
 #pragma unroll
@@ -504,9 +537,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
             __syncwarp();
             if (task) {
                 const int q = q0 + kq;
-                if (do_eval)
-#pragma unroll
-                    for (int k = 0; k < M; ++k) sm.cells[kq * VR + 3 * k + kch] = rc[k];
+                if (do_eval) store_cells<M>(sm.cells, kq, kch, rc);
                 if (need_coef) sm.vtot[kq * 3 + kch] = (double)expf(-rc[M - 1]);  // A(z -> 1) = v_{M-1}
                 // coefficients: Haar analysis of v in f64 (wavelet.py:3-9 layout):
                 // c[2^n + k] = 2^(n/2)/M (sum left half - sum right half), c[0] = mean
@@ -567,8 +598,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
                     if (do_eval) {
                         double cell[S];
                         haar_cells<R>(c, cell);
-#pragma unroll
-                        for (int s = 0; s < S; ++s) sm.cells[kq * VR + 3 * s + kch] = (float)cell[s];
+                        store_cells<M>(sm.cells, kq, kch, cell);
                     }
                 }
             }
@@ -585,8 +615,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
                 sm.vtot[kq * 3 + kch] = (double)expf(-(float)fmax(at, 0.0));
                 double cell[S];
                 haar_cells<R>(c, cell);
-#pragma unroll
-                for (int s = 0; s < S; ++s) sm.cells[kq * VR + 3 * s + kch] = (float)cell[s];
+                store_cells<M>(sm.cells, kq, kch, cell);
             }
         }
         fence_proxy_async();  // coef32 becomes visible to the bulk store
@@ -607,7 +636,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
         // ---- 6. evaluate (step3): v̂ per fragment, chunk accumulators --------------
         if (do_eval) {
             if (lane < C) {
-                const float* cqv = sm.cells + cq * VR;
+                const float2* cq2 = sm.cells + cq * CellRow<M>::CR;
                 float ac[3] = {0.f, 0.f, 0.f}, wg[3] = {0.f, 0.f, 0.f};
                 double ro[2] = {0.0, 0.0};
                 double d[3] = {0.0, 0.0, 0.0}, topq = INFINITY;
@@ -616,15 +645,17 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
                     ray_dir(kp, kp.f.pixel_base + p, d);
                     topq = kp.f.opaque_depth ? (double)kp.f.opaque_depth[p] : INFINITY;
                 }
+                const bool op_staged = ph & PH_BUILD;  // the build left alpha (1 - T') in the trans slot
                 int jj = crot;
 #pragma unroll kUnroll
                 for (int j = 0; j < clen; ++j) {
                     const int fr = cst + jj;
                     jj = jj + 1 == clen ? 0 : jj + 1;
                     const int si = sh4 + fr;
-                    int c0, c1;
+                    int c0;
                     float t;
-                    eval_cells(sm.zfix[fr], R, c0, c1, t);
+                    eval_cell(sm.zfix[fr], R, c0, t);
+                    const float2* cv = cq2 + c0 * 3;
                     const float al = sm.alpha[si];
                     bool cb_ = false;
                     float io = 1.0f;
@@ -634,11 +665,14 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
                     }
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) {
-                        const float A = fmaxf((1.0f - t) * cqv[c0 * 3 + ch] + t * cqv[c1 * 3 + ch], 0.0f);
+                        // A = lerp of the two neighbouring cell centres, clamped >= 0 (wavelet.py:316-319)
+                        const float2 vd = cv[ch];
+                        const float A = fmaxf(fmaf(t, vd.y, vd.x), 0.0f);
                         const float vh = __expf(-A);
                         const float Lr = sm.rad[3 * si + ch];
+                        const float op = op_staged ? sm.trans[3 * si + ch] : opacity_ch(al, sm.trans[3 * si + ch], cb_);
                         ac[ch] += (Lr * al) * vh;
-                        wg[ch] += opacity_ch(al, sm.trans[3 * si + ch], cb_) * vh;
+                        wg[ch] += op * vh;
                         sm.rad[3 * si + ch] = vh;  // v̂ replaces radiance in place
                     }
                     if (refr && io > 1.0f) {

@@ -44,7 +44,7 @@ struct WT {
     static constexpr int CH = 8;             // fragments per chunk (max)
     static constexpr int FBW = 32 * CH;      // fragments per warp sub-tile (max)
     static constexpr int WIN = 32;           // pixels per warp window
-    static constexpr int SUBP = 10;          // pixels per sub-tile (3 SUBP <= 32 (pixel, channel) tasks)
+    static constexpr int SUBP = 8;           // pixels per sub-tile (3 SUBP <= 32 (pixel, channel) tasks)
     static constexpr int WPB = R <= 3 ? WOIT_WPB : 1;  // warps per CTA
     static constexpr int VR = V + ((35 - V % 32) % 32);  // row stride == 3 (mod 32), >= V
 };
@@ -92,11 +92,12 @@ WOIT_HD WLayout make_wlayout(uint32_t phases, int flags) {
     // build, then the sub-tile's coefficients [SUBP][V], cell staircase [SUBP][VR]
     // and chunk accumulators [8][32]
     const uint32_t part_b = (phases & PH_BUILD) ? 4u * G::V * 32 : 0u;
-    const uint32_t after_b = 4u * G::SUBP * G::V + 4u * G::SUBP * G::VR + (ev ? 4u * 8 * 32 : 0u);
+    const uint32_t CR = 3u * G::S + ((3u + 16u * 64u - 3u * G::S) % 16u);  // frame.cu CellRow
+    const uint32_t after_b = align16(4u * G::SUBP * G::V) + align16(8u * G::SUBP * CR) + (ev ? 4u * 8 * 32 : 0u);
     L.part = o;  o = align16(o + (part_b > after_b ? part_b : after_b));
     L.coef32 = L.part;
     L.cells = L.part + align16(4u * G::SUBP * G::V);
-    L.accp = L.cells + align16(4u * G::SUBP * G::VR);
+    L.accp = L.cells + align16(8u * G::SUBP * CR);
     L.pk = o;    o = align16(o + (packed ? 8u * G::WIN * G::V : 0u));
     L.opq = o;   o = align16(o + 12u * (G::SUBP + 8));
     L.bar = o;   o = align16(o + 16u);

@@ -10,7 +10,7 @@
 #include "packing.cuh"
 
 #ifndef WOIT_WPB
-#define WOIT_WPB 2
+#define WOIT_WPB 1
 #endif
 
 namespace woit {

@@ -376,14 +376,11 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
             const int nc = sm.nch[q];
             const int base = sm.cb[q] - sm.cb[q0];
             const int rel = (int)(sm.offs[q] - fa);
-            if (nc > 0) {
-                const int len0 = run / nc, extra = run - len0 * nc;
-                int st = rel;
-                for (int i = 0; i < nc; ++i) {
-                    const int len = len0 + (i < extra ? 1 : 0);
-                    sm.chunk[base + i] = pack_chunk(lane, st, len);
-                    st += len;
-                }
+            // chunk i of the pixel = fragments [CH i, min(CH (i+1), run)): a function of
+            // the run length only, so the reduction order never depends on the tiling
+            for (int i = 0; i < nc; ++i) {
+                const int st = i * CH;
+                sm.chunk[base + i] = pack_chunk(lane, rel + st, run - st < CH ? run - st : CH);
             }
             const int64_t p = w0 + q;
             const bool init_empty = (ph & PH_BOUNDS) && !(ph & PH_BOUNDS_ACC);
@@ -716,7 +713,40 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
         }
 
         // ---- 7. per-pixel accumulators + composite (step4) -------------------------
-        if (lane < nqs) {
+        if (!GEN) {
+            // fast path: one lane per (pixel, channel) -- the channels are independent
+            if (lane < 3 * nqs) {
+                const int kch = lane / nqs, kq = lane - kch * nqs;
+                const int q = q0 + kq;
+                const int64_t p = w0 + q;
+                const int nc = sm.nch[q];
+                const int cbq = sm.cb[q] - sm.cb[q0];
+                double acc = 0.0, wgt = 0.0;
+                for (int i = 0; i < nc; ++i) {
+                    acc += (double)sm.accp[kch * WC + cbq + i];
+                    wgt += (double)sm.accp[(3 + kch) * WC + cbq + i];
+                }
+                if (kp.b.accum) kp.b.accum[p * 3 + kch] = (float)acc;
+                if (kp.b.weight) kp.b.weight[p * 3 + kch] = (float)wgt;
+                if (kp.b.output) {
+                    const int si = (int)(p - ((w0 + q0) & ~(int64_t)3));
+                    const double bg = (double)sm.opq[3 * si + kch];
+                    const double vt = sm.vtot[kq * 3 + kch];
+                    double o;
+                    if (flags & WOIT_NORMALIZE) {
+                        const double avg = acc * rcp_refined(fmax(kNormEps, wgt));
+                        o = dadd(dmul(avg, 1.0 - vt), dmul(bg, vt));
+                    } else {
+                        o = dadd(acc, dmul(bg, vt));
+                    }
+                    kp.b.output[p * 3 + kch] = (float)o;
+                }
+                if (kch == 0 && kp.b.refraction_offset) {
+                    kp.b.refraction_offset[p * 2] = 0.0f;
+                    kp.b.refraction_offset[p * 2 + 1] = 0.0f;
+                }
+            }
+        } else if (lane < nqs) {
             const int q = q0 + lane;
             const int64_t p = w0 + q;
             double acc[3] = {0, 0, 0}, wgt[3] = {0, 0, 0}, ro[2] = {0, 0};

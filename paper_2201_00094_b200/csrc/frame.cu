@@ -130,6 +130,68 @@ WOIT_D void store_cells(float2* cells, int kq, int kch, const TV v[M]) {
     }
 }
 
+// Fast-path chunk loops as functions with __restrict__ parameters: the compiler may
+// then move the loads of later fragments above the shared-memory stores of earlier
+// ones (the pointers provably do not alias), which it cannot do in the kernel body.
+template <int R>
+WOIT_D void build_chunk_fast(const zfix_t* __restrict__ zf, const float* __restrict__ alp,
+                             float* __restrict__ trs, float* __restrict__ part, int lane, int cst,
+                             int clen, int crot, int sh4) {
+    constexpr int M = 2 << R, WC = 32;
+    int jj = crot;
+#pragma unroll kUnroll
+    for (int j = 0; j < clen; ++j) {
+        const int fr = cst + jj;
+        jj = jj + 1 == clen ? 0 : jj + 1;
+        const int si = sh4 + fr;
+        const zfix_t zi = zf[fr];
+        const float al = alp[si];
+        float a[3];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            const float op = opacity_ch(al, trs[3 * si + ch], false);
+            trs[3 * si + ch] = op;  // the evaluation's weight 1 - t (pipeline.py:184)
+            a[ch] = -log_poly(fmaxf((float)kTransFloor, 1.0f - op));
+        }
+        const int cell = (int)(zi >> (kZBits - (R + 1)));
+        const float fr_ = u32_to_unit(zi << (R + 1), kZBits);  // M z - j_f
+        float* d = part + cell * 3 * WC + lane;
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) d[ch * WC] += a[ch] * (1.0f - fr_);
+        if (cell + 1 < M)
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) d[(3 + ch) * WC] += a[ch] * fr_;
+    }
+}
+
+template <int R>
+WOIT_D void eval_chunk_fast(const zfix_t* __restrict__ zf, const float* __restrict__ alp,
+                            const float* __restrict__ opw, const float2* __restrict__ cq2,
+                            float* __restrict__ rad, int cst, int clen, int crot, int sh4, float ac[3],
+                            float wg[3]) {
+    int jj = crot;
+#pragma unroll kUnroll
+    for (int j = 0; j < clen; ++j) {
+        const int fr = cst + jj;
+        jj = jj + 1 == clen ? 0 : jj + 1;
+        const int si = sh4 + fr;
+        int c0;
+        float t;
+        eval_cell(zf[fr], R, c0, t);
+        const float2* cv = cq2 + c0 * 3;
+        const float al = alp[si];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            const float2 vd = cv[ch];
+            const float A = fmaxf(fmaf(t, vd.y, vd.x), 0.0f);
+            const float vh = exp_neg(A);
+            ac[ch] += (rad[3 * si + ch] * al) * vh;
+            wg[ch] += opw[3 * si + ch] * vh;
+            rad[3 * si + ch] = vh;  // v̂ replaces radiance in place
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // The fused frame kernel. Every warp owns a window of WIN consecutive pixels and
 // processes it in sub-tiles of <= 32 chunks (<= 256 fragments) on its own slice
@@ -456,7 +518,9 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
                 for (int i = lane; i < (M * 3 * WC) / 4; i += 32) pz[i] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
             __syncwarp();
-            if (lane < C) {
+            if (!GEN && lane < C) {
+                build_chunk_fast<R>(sm.zfix, sm.alpha, sm.trans, part, lane, cst, clen, crot, sh4);
+            } else if (lane < C) {
                 int jj = crot;
 #pragma unroll kUnroll
                 for (int j = 0; j < clen; ++j) {
@@ -643,6 +707,9 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
                     topq = kp.f.opaque_depth ? (double)kp.f.opaque_depth[p] : INFINITY;
                 }
                 const bool op_staged = ph & PH_BUILD;  // the build left alpha (1 - T') in the trans slot
+                if (!GEN) {
+                    eval_chunk_fast<R>(sm.zfix, sm.alpha, sm.trans, cq2, sm.rad, cst, clen, crot, sh4, ac, wg);
+                } else {
                 int jj = crot;
 #pragma unroll kUnroll
                 for (int j = 0; j < clen; ++j) {
@@ -665,7 +732,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
                         // A = lerp of the two neighbouring cell centres, clamped >= 0 (wavelet.py:316-319)
                         const float2 vd = cv[ch];
                         const float A = fmaxf(fmaf(t, vd.y, vd.x), 0.0f);
-                        const float vh = __expf(-A);
+                        const float vh = exp_neg(A);
                         const float Lr = sm.rad[3 * si + ch];
                         const float op = op_staged ? sm.trans[3 * si + ch] : opacity_ch(al, sm.trans[3 * si + ch], cb_);
                         ac[ch] += (Lr * al) * vh;
@@ -679,6 +746,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
                         ro[0] += off[0];
                         ro[1] += off[1];
                     }
+                }
                 }
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) {

@@ -135,8 +135,8 @@ WOIT_D void store_cells(float2* cells, int kq, int kch, const TV v[M]) {
 // ones (the pointers provably do not alias), which it cannot do in the kernel body.
 template <int R>
 WOIT_D void build_chunk_fast(const zfix_t* __restrict__ zf, const float* __restrict__ alp,
-                             float* __restrict__ trs, float* __restrict__ part, int lane, int cst,
-                             int clen, int crot, int sh4) {
+                             float* __restrict__ trs, float* __restrict__ part, float* __restrict__ sink,
+                             int lane, int cst, int clen, int crot, int sh4) {
     constexpr int M = 2 << R, WC = 32;
     int jj = crot;
 #pragma unroll kUnroll
@@ -156,11 +156,13 @@ WOIT_D void build_chunk_fast(const zfix_t* __restrict__ zf, const float* __restr
         const int cell = (int)(zi >> (kZBits - (R + 1)));
         const float fr_ = u32_to_unit(zi << (R + 1), kZBits);  // M z - j_f
         float* d = part + cell * 3 * WC + lane;
+        // D_{j+1} of the last cell lies past the staircase: a select into a scratch
+        // row instead of a divergent branch
+        float* d2 = cell + 1 < M ? d + 3 * WC : sink;
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) d[ch * WC] += a[ch] * (1.0f - fr_);
-        if (cell + 1 < M)
 #pragma unroll
-            for (int ch = 0; ch < 3; ++ch) d[(3 + ch) * WC] += a[ch] * fr_;
+        for (int ch = 0; ch < 3; ++ch) d2[ch * WC] += a[ch] * fr_;
     }
 }
 
@@ -486,21 +488,21 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
             const DepthMap m = depth_map(nf, ff, R);
             sm.lo[lane] = m.lo;
             sm.den[lane] = m.den;
-            sm.rcp[lane] = m.rcp;
+            sm.rcp[lane] = m.rs;  // fixed-point z scale (z_fixed_of)
         }
         __syncwarp();
 
         // ---- 4. z (fixed point) and build (step2): chunk partials -> part[v][lane] ----
         float* part = sm.part;
         if (lane < C && do_at) {
-            const DepthMap m{sm.lo[cq], sm.den[cq], sm.rcp[cq]};
+            const DepthMap m{sm.lo[cq], sm.den[cq], 0.0, sm.rcp[cq]};
 #pragma unroll kZUnroll
             for (int j = 0; j < CH; ++j) {  // independent chains: unrolled for ILP
                 if (j < clen) {
                     int jj = crot + j;
                     jj = jj >= clen ? jj - clen : jj;
                     const int fr = cst + jj;
-                    sm.zfix[fr] = z_fixed(normalized_z(sm.depth[sh4 + fr], m));
+                    sm.zfix[fr] = z_fixed_of(sm.depth[sh4 + fr], m);
                 }
             }
         }
@@ -518,8 +520,10 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
                 for (int i = lane; i < (M * 3 * WC) / 4; i += 32) pz[i] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
             __syncwarp();
+            // scratch [3][32] for the dropped D_M terms: vtot is dead until phase 5
+            float* sink = reinterpret_cast<float*>(sm.vtot) + lane;
             if (!GEN && lane < C) {
-                build_chunk_fast<R>(sm.zfix, sm.alpha, sm.trans, part, lane, cst, clen, crot, sh4);
+                build_chunk_fast<R>(sm.zfix, sm.alpha, sm.trans, part, sink, lane, cst, clen, crot, sh4);
             } else if (lane < C) {
                 int jj = crot;
 #pragma unroll kUnroll
@@ -541,11 +545,11 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
                     const int cell = (int)(zi >> (kZBits - (R + 1)));
                     const float fr_ = u32_to_unit(zi << (R + 1), kZBits);  // M z - j_f
                     float* d = part + cell * 3 * WC + lane;
+                    float* d2 = cell + 1 < M ? d + 3 * WC : sink;
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) d[ch * WC] += a[ch] * (1.0f - fr_);
-                    if (cell + 1 < M)
 #pragma unroll
-                        for (int ch = 0; ch < 3; ++ch) d[(3 + ch) * WC] += a[ch] * fr_;
+                    for (int ch = 0; ch < 3; ++ch) d2[ch * WC] += a[ch] * fr_;
                 }
             }
             __syncwarp();
@@ -939,8 +943,7 @@ __global__ void __launch_bounds__(kLongT) long_pixel_kernel(const KParams kp) {
             if (tid < TL) {
                 for (int v = 0; v < V; ++v) acc64[v * TL + tid] = 0.0;
                 for (int64_t f = s + tid; f < e; f += TL) {
-                    const double z = normalized_z(kp.f.depth[f], m);
-                    const zfix_t zi = z_fixed(z);
+                    const zfix_t zi = z_fixed_of(kp.f.depth[f], m);
                     const float al = kp.f.alpha[f];
                     bool cb_ = false;
                     if (cube) {
@@ -1010,7 +1013,7 @@ __global__ void __launch_bounds__(kLongT) long_pixel_kernel(const KParams kp) {
                 topq = kp.f.opaque_depth ? (double)kp.f.opaque_depth[p] : INFINITY;
             }
             for (int64_t f = s + tid; f < e; f += kLongT) {
-                const zfix_t zi = z_fixed(normalized_z(kp.f.depth[f], m));
+                const zfix_t zi = z_fixed_of(kp.f.depth[f], m);
                 int c0, c1;
                 float t;
                 eval_cells(zi, R, c0, c1, t);
@@ -1168,7 +1171,7 @@ __global__ void indices_kernel(const KParams kp, double* z_out, int32_t* k_out, 
         const DepthMap m = depth_map(kp.b.near[p], kp.b.far[p], rank);
         for (int64_t f = kp.f.offsets[p]; f < kp.f.offsets[p + 1]; ++f) {
             const double z = normalized_z(kp.f.depth[f], m);
-            const zfix_t zi = z_fixed(z);
+            const zfix_t zi = z_fixed_of(kp.f.depth[f], m);
             z_out[f] = z;
             for (int n = 0; n <= rank; ++n) k_out[f * (rank + 1) + n] = slot_offset(zi, n);
             int c0, c1;

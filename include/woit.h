@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define WOIT_ABI_VERSION 1
+#define WOIT_ABI_VERSION 2
 
 /* status codes */
 #define WOIT_OK 0
@@ -60,6 +60,17 @@ extern "C" {
 #define WOIT_PACKED_STORAGE 0x10
 #define WOIT_LITERAL_SPECTRAL_T 0x20
 #define WOIT_CUBE_BACKFACE_ONLY 0x40
+/* Diffusion ("resolve and blur", BASELINE north star (3)-(4)). The reference has no
+ * such pass, so this is the IN-REPO definition, parity unpinned:
+ *   step3 also accumulates the pixel's visibility-weighted coverage
+ *       D_p = sum_f alpha_f * (vhat_f.r + vhat_f.g + vhat_f.b) / 3      (bufs->diffusion)
+ *   K_resolve blurs the background image with a separable, edge-clamped Gaussian of
+ *       `diffusion_radius` taps each side, sigma = radius / 2 (woit_resolve_blur);
+ *   step4 replaces the background bg by bg + w (bg_blurred - bg), w = min(1, diffusion * D_p),
+ *       bg_blurred sampled from the blurred image exactly as bg is from the sharp one.
+ * Off by default; with the flag clear every output is bit-identical to a build
+ * without this feature. */
+#define WOIT_DIFFUSION 0x80
 
 typedef struct woit_frags {
     int32_t width;        /* full frame width  (RenderConfig.width)  */
@@ -84,13 +95,14 @@ typedef struct woit_params {
     int32_t rank;            /* N, 0..6 */
     int32_t flags;           /* WOIT_* booleans */
     int32_t aberration_taps; /* odd, >= 3 */
-    int32_t reserved;
+    int32_t diffusion_radius; /* WOIT_DIFFUSION: blur taps each side, 1..64 */
     double refraction_scale; /* pixels per world unit at width 512 */
     double cam_forward[3];   /* Camera.basis() (scene.py:141-150) */
     double cam_right[3];
     double cam_up[3];
     double tan_half;         /* tan(fov/2) (scene.py:201) */
     double aspect;           /* width / height */
+    double diffusion;        /* WOIT_DIFFUSION: strength (>= 0), w = min(1, diffusion * D_p) */
 } woit_params_t;
 
 typedef struct woit_bufs {
@@ -104,6 +116,9 @@ typedef struct woit_bufs {
     float* vhat;               /* per-fragment transmittance; NULL: not written */
     const float* full_opaque_image; /* [height][width][3] for refraction / aberration gathers;
                                        NULL: the band's opaque_color with pixel_base 0 */
+    float* diffusion;          /* [npix] coverage D_p (WOIT_DIFFUSION); NULL: not written */
+    const float* blurred_image; /* WOIT_DIFFUSION: woit_resolve_blur of the background image,
+                                   same extent/indexing as the image bg is read from */
 } woit_bufs_t;
 
 /* ---- version / errors ---------------------------------------------------- */
@@ -147,6 +162,16 @@ int woit_step4_composite(const woit_frags_t* frags, const woit_params_t* params,
  * frame kernels use, from bufs near/far. For bit-exact index parity checks. */
 int woit_fragment_indices(const woit_frags_t* frags, const float* near, const float* far, int rank,
                           double* z, int32_t* slots, int32_t* cells, void* stream);
+
+/* ---- K_resolve: the diffusion blur (in-repo definition, see WOIT_DIFFUSION) ----- */
+
+size_t woit_blur_workspace_bytes(int32_t width, int32_t height);
+
+/* out = separable Gaussian blur of image (float [height][width][3]), edge clamped,
+ * taps -radius..radius with weights exp(-i^2 / (2 sigma^2)) / sum, sigma = radius / 2:
+ * a horizontal then a vertical pass, both with 128-bit coalesced loads/stores. */
+int woit_resolve_blur(const float* image, int32_t width, int32_t height, int32_t radius,
+                      float* out, void* ws, size_t ws_bytes, void* stream);
 
 /* ---- batch kernels (wavelet.py:272-337) ------------------------------------
  * Same dtypes as the reference (float64 throughout). With WOIT_BUILD_BINNED the

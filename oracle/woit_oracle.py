@@ -129,6 +129,8 @@ class OConfig:
     workers: int = 1
     literal_spectral_t: bool = False
     cube_backface_only: bool = False
+    diffusion: float = 0.0        # in-repo diffusion (no reference twin; see blur_image)
+    diffusion_radius: int = 4
 
 
 @dataclass(frozen=True)
@@ -310,6 +312,7 @@ class OBuffers:
     opaque_color: np.ndarray
     output: np.ndarray
     vhat: Optional[np.ndarray] = field(default=None)
+    diffusion: Optional[np.ndarray] = field(default=None)
 
     @classmethod
     def allocate(cls, frame: OFrame, rank: int) -> "OBuffers":
@@ -317,7 +320,7 @@ class OBuffers:
         return cls(frame.width, frame.height, rank, np.full(P, np.inf), np.full(P, -np.inf),
                    np.zeros((P, 1 << (rank + 1), 3)), np.zeros((P, 3)), np.zeros((P, 3)),
                    np.zeros((P, 2)), frame.opaque_depth.copy(), frame.opaque_color.copy(),
-                   np.zeros((P, 3)))
+                   np.zeros((P, 3)), None, np.zeros(P))
 
 
 def fragment_z(frame: OFrame, bufs: OBuffers) -> np.ndarray:
@@ -361,6 +364,9 @@ def step3_accumulate(dirs: np.ndarray, forward, right, up, frame: OFrame, bufs: 
     np.add.at(bufs.accum, frame.pixel, frame.radiance * frame.alpha[:, None] * vhat)
     opac = 1.0 - frame.net_transmittance(cfg.cube_transmission, cfg.cube_backface_only)
     np.add.at(bufs.accum_weight, frame.pixel, opac * vhat)
+    if cfg.diffusion > 0.0:
+        # in-repo diffusion coverage D_p = sum alpha * mean(v̂) (include/woit.h WOIT_DIFFUSION)
+        np.add.at(bufs.diffusion, frame.pixel, frame.alpha * vhat.sum(axis=1) / 3.0)
     if not cfg.refraction:
         return
     sel = np.nonzero(frame.ior > 1.0)[0]
@@ -431,21 +437,63 @@ def chromatic_gather(img, px, py, offset, k, literal_t=False):
     return np.where(safe, num / np.where(safe, den, 1.0), center)
 
 
-def step4_composite(bufs: OBuffers, cfg: OConfig, pixel_base: int = 0, full_img=None) -> None:
-    """Blend over the (refracted / aberrated) background (pipeline.py:284-308)."""
+def gaussian_taps(radius: int) -> np.ndarray:
+    """In-repo diffusion blur weights (no reference twin): exp(-i^2 / (2 sigma^2)),
+    sigma = radius / 2, i = -radius..radius, normalised to sum 1 (include/woit.h)."""
+    sigma = 0.5 * radius
+    i = np.arange(-radius, radius + 1, dtype=np.float64)
+    g = np.exp(-(i * i) / (2.0 * sigma * sigma))
+    return g / g.sum()
+
+
+def blur_image(img, radius: int) -> np.ndarray:
+    """K_resolve twin: separable edge-clamped Gaussian, rows then columns, f64."""
+    img = np.asarray(img, dtype=np.float64)
+    H, W = img.shape[:2]
+    g = gaussian_taps(radius)
+    xs = np.arange(W)
+    ys = np.arange(H)
+    tmp = np.zeros_like(img)
+    for k, w in zip(range(-radius, radius + 1), g):
+        tmp += w * img[:, np.clip(xs + k, 0, W - 1)]
+    out = np.zeros_like(img)
+    for k, w in zip(range(-radius, radius + 1), g):
+        out += w * tmp[np.clip(ys + k, 0, H - 1)]
+    return out
+
+
+def _background(img, bufs: OBuffers, cfg: OConfig, px, py, own):
+    """Background sample (pipeline.py:290-303) of ``img``; ``own`` = the pixels' own colours."""
+    if cfg.chromatic_aberration:
+        return chromatic_gather(img, px, py, bufs.refraction_offset, cfg.aberration_taps,
+                                cfg.literal_spectral_t)
+    if cfg.refraction:
+        return bilinear_sample(img, px + bufs.refraction_offset[:, 0],
+                               py + bufs.refraction_offset[:, 1])
+    return own
+
+
+def step4_composite(bufs: OBuffers, cfg: OConfig, pixel_base: int = 0, full_img=None,
+                    blurred_img=None) -> None:
+    """Blend over the (refracted / aberrated) background (pipeline.py:284-308).
+
+    With ``cfg.diffusion > 0`` (in-repo, no reference twin) the background is
+    lerped towards the same sample of the blurred image by min(1, diffusion * D_p).
+    """
     v_total = np.exp(-total_absorbance_batch(bufs.coeffs, bufs.rank))
     img = bufs.opaque_color.reshape(-1, bufs.width, 3) if full_img is None else full_img
     gp = pixel_base + np.arange(bufs.near.size)
     px = (gp % bufs.width).astype(np.float64)
     py = (gp // bufs.width).astype(np.float64)
-    if cfg.chromatic_aberration:
-        bg = chromatic_gather(img, px, py, bufs.refraction_offset, cfg.aberration_taps,
-                              cfg.literal_spectral_t)
-    elif cfg.refraction:
-        bg = bilinear_sample(img, px + bufs.refraction_offset[:, 0],
-                             py + bufs.refraction_offset[:, 1])
-    else:
-        bg = bufs.opaque_color
+    bg = _background(img, bufs, cfg, px, py, bufs.opaque_color)
+    if cfg.diffusion > 0.0:
+        if blurred_img is None:
+            blurred_img = blur_image(img, cfg.diffusion_radius)
+        base = full_img is not None
+        own = blurred_img.reshape(-1, 3)[gp if base else np.arange(bufs.near.size)]
+        bb = _background(blurred_img, bufs, cfg, px, py, own)
+        w = np.minimum(1.0, cfg.diffusion * bufs.diffusion)[:, None]
+        bg = bg + w * (bb - bg)
     if cfg.normalize:
         bufs.output[:] = bufs.accum / np.maximum(NORM_EPS, bufs.accum_weight) * (1.0 - v_total) \
             + bg * v_total
@@ -454,7 +502,7 @@ def step4_composite(bufs: OBuffers, cfg: OConfig, pixel_base: int = 0, full_img=
 
 
 def render_band(frame: OFrame, cfg: OConfig, cam: OCamera, full_img, p0: int, p1: int,
-                dirs=None) -> OBuffers:
+                dirs=None, blurred_img=None) -> OBuffers:
     """One row band through the four passes (pipeline.py:321-330)."""
     band = frame if (p0, p1) == (0, frame.npix) else frame.band(p0, p1)
     if dirs is None and cfg.refraction:
@@ -464,7 +512,7 @@ def render_band(frame: OFrame, cfg: OConfig, cam: OCamera, full_img, p0: int, p1
     step1_depth_bounds(band, bufs)
     step2_build(band, bufs, cfg)
     step3_accumulate(dirs, f, r, u, band, bufs, cfg, pixel_base=p0)
-    step4_composite(bufs, cfg, pixel_base=p0, full_img=full_img)
+    step4_composite(bufs, cfg, pixel_base=p0, full_img=full_img, blurred_img=blurred_img)
     return bufs
 
 
@@ -479,18 +527,20 @@ def render_frame(frame: OFrame, cfg: OConfig, cam: OCamera = OCamera(),
     workers = cfg.workers if workers is None else workers
     full_img = frame.opaque_color.reshape(H, W, 3)
     dirs = ray_dirs(cam, W, H) if cfg.refraction else None
+    blurred = blur_image(full_img, cfg.diffusion_radius) if cfg.diffusion > 0.0 else None
     if workers == 1 or H < 2 * workers:
-        return render_band(frame, cfg, cam, full_img, 0, frame.npix, dirs)
+        return render_band(frame, cfg, cam, full_img, 0, frame.npix, dirs, blurred)
     rows = np.linspace(0, H, workers + 1).astype(int)
     spans = [(rows[i] * W, rows[i + 1] * W) for i in range(workers) if rows[i] < rows[i + 1]]
     with ThreadPoolExecutor(max_workers=len(spans)) as pool:
-        parts = list(pool.map(lambda s: render_band(frame, cfg, cam, full_img, s[0], s[1], dirs),
-                              spans))
+        parts = list(pool.map(lambda s: render_band(frame, cfg, cam, full_img, s[0], s[1], dirs,
+                                                    blurred), spans))
     cat = lambda name: np.concatenate([getattr(b, name) for b in parts], axis=0)
     out = OBuffers(W, H, cfg.rank, cat("near"), cat("far"), cat("coeffs"), cat("accum"),
                    cat("accum_weight"), cat("refraction_offset"), cat("opaque_depth"),
                    cat("opaque_color"), cat("output"))
     out.vhat = cat("vhat")
+    out.diffusion = cat("diffusion")
     return out
 
 

@@ -14,7 +14,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # WOIT_LIB selects an alternative build (tuning variants, tools/variants.py)
 LIB_PATH = os.environ.get("WOIT_LIB") or os.path.join(_HERE, "libwoit.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 OK = 0
 EINVAL = -1
@@ -30,6 +30,7 @@ NORMALIZE = 0x08
 PACKED_STORAGE = 0x10
 LITERAL_SPECTRAL_T = 0x20
 CUBE_BACKFACE_ONLY = 0x40
+DIFFUSION = 0x80
 
 BUILD_BINNED = 0
 BUILD_ATOMIC = 1
@@ -50,16 +51,16 @@ class Frags(C.Structure):
 
 
 class Params(C.Structure):
-    _fields_ = [("rank", _i32), ("flags", _i32), ("aberration_taps", _i32), ("reserved", _i32),
+    _fields_ = [("rank", _i32), ("flags", _i32), ("aberration_taps", _i32), ("diffusion_radius", _i32),
                 ("refraction_scale", C.c_double), ("cam_forward", C.c_double * 3),
                 ("cam_right", C.c_double * 3), ("cam_up", C.c_double * 3),
-                ("tan_half", C.c_double), ("aspect", C.c_double)]
+                ("tan_half", C.c_double), ("aspect", C.c_double), ("diffusion", C.c_double)]
 
 
 class Bufs(C.Structure):
     _fields_ = [("near", _vp), ("far", _vp), ("coeffs", _vp), ("accum", _vp), ("weight", _vp),
                 ("refraction_offset", _vp), ("output", _vp), ("vhat", _vp),
-                ("full_opaque_image", _vp)]
+                ("full_opaque_image", _vp), ("diffusion", _vp), ("blurred_image", _vp)]
 
 
 _SIGS = {
@@ -73,6 +74,8 @@ _SIGS = {
                                         _vp]),
     "woit_step4_composite": (C.c_int, [C.POINTER(Frags), C.POINTER(Params), C.POINTER(Bufs), _vp]),
     "woit_fragment_indices": (C.c_int, [C.POINTER(Frags), _vp, _vp, C.c_int, _vp, _vp, _vp, _vp]),
+    "woit_blur_workspace_bytes": (_sz, [_i32, _i32]),
+    "woit_resolve_blur": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _vp, _sz, _vp]),
     "woit_build_into_workspace_bytes": (_sz, [_i64, _i64]),
     "woit_build_into": (C.c_int, [_vp, _i64, _vp, _vp, _vp, _i64, C.c_int, C.c_int, _vp, _sz, _vp]),
     "woit_interp_absorbance": (C.c_int, [_vp, _i64, _vp, _vp, _i64, C.c_int, _vp, _vp]),

@@ -1,5 +1,7 @@
 // extern "C" entry points of libwoit.so (declared in include/woit.h): argument
 // validation, workspace carving and launch. No allocation, no global state.
+#include <cmath>
+
 #include "frame.cuh"
 #include "internal.cuh"
 
@@ -7,7 +9,8 @@ using namespace woit;
 
 namespace {
 
-constexpr int64_t kMinFB = 256;  // smallest sub-tile (rank 6): bounds the long-pixel list
+constexpr int64_t kMinFB = 256;
+constexpr int kMaxDiffusionRadius = 64;  // smallest sub-tile (rank 6): bounds the long-pixel list
 
 int64_t long_cap(int64_t nfrag) { return nfrag / (kMinFB + 1) + 2; }
 
@@ -19,6 +22,10 @@ int check_params(const woit_params_t* p) {
     if (!p) return WOIT_EINVAL;
     if (p->rank < 0 || p->rank > kMaxRank) return WOIT_ERANK;
     if (p->aberration_taps < 3 || (p->aberration_taps % 2) == 0) return WOIT_ETAPS;
+    if ((p->flags & WOIT_DIFFUSION) &&
+        (!(p->diffusion >= 0.0) || !std::isfinite(p->diffusion) || p->diffusion_radius < 1 ||
+         p->diffusion_radius > kMaxDiffusionRadius))
+        return WOIT_EINVAL;
     return WOIT_OK;
 }
 
@@ -37,6 +44,7 @@ int run_frame(const woit_frags_t* f, const woit_params_t* p, woit_bufs_t* b, uin
     if (f->npix == 0) return WOIT_OK;
     if (ws_bytes < woit_frame_workspace_bytes(f->npix, f->nfrag) || !ws) return WOIT_EWORKSPACE;
     if ((phases & PH_COMPOSITE) && (!b->output || !f->opaque_color)) return WOIT_EINVAL;
+    if ((phases & PH_COMPOSITE) && (p->flags & WOIT_DIFFUSION) && !b->blurred_image) return WOIT_EINVAL;
     if ((phases & (PH_BOUNDS_ACC)) && (!b->near || !b->far)) return WOIT_EINVAL;
     if (!(phases & PH_BOUNDS) && (!b->near || !b->far)) return WOIT_EINVAL;
     if ((phases & PH_BUILD_ACC) && !b->coeffs) return WOIT_EINVAL;
@@ -139,6 +147,7 @@ int woit_step4_composite(const woit_frags_t* frags, const woit_params_t* params,
     if (!frags || frags->width < 1 || frags->height < 1 || frags->npix < 0) return WOIT_EINVAL;
     if (!bufs || !bufs->coeffs || !bufs->accum || !bufs->weight || !bufs->output || !frags->opaque_color)
         return WOIT_EINVAL;
+    if ((params->flags & WOIT_DIFFUSION) && (!bufs->blurred_image || !bufs->diffusion)) return WOIT_EINVAL;
     KParams kp;
     kp.f = *frags;
     kp.p = *params;
@@ -161,6 +170,18 @@ int woit_fragment_indices(const woit_frags_t* frags, const float* near, const fl
     kp.b.near = const_cast<float*>(near);
     kp.b.far = const_cast<float*>(far);
     return cuda_status(launch_indices(kp, z, slots, cells, static_cast<cudaStream_t>(stream)));
+}
+
+size_t woit_blur_workspace_bytes(int32_t width, int32_t height) {
+    return width < 1 || height < 1 ? 0 : blur_workspace(width, height);
+}
+
+int woit_resolve_blur(const float* image, int32_t width, int32_t height, int32_t radius, float* out, void* ws,
+                      size_t ws_bytes, void* stream) {
+    if (!image || !out || width < 1 || height < 1) return WOIT_EINVAL;
+    if (radius < 1 || radius > kMaxDiffusionRadius) return WOIT_EINVAL;
+    if (!ws || ws_bytes < blur_workspace(width, height)) return WOIT_EWORKSPACE;
+    return cuda_status(resolve_blur(image, width, height, radius, out, ws, static_cast<cudaStream_t>(stream)));
 }
 
 size_t woit_build_into_workspace_bytes(int64_t n, int64_t npix) { return build_into_workspace(n, npix); }

@@ -290,6 +290,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
     const bool do_eval = ph & PH_EVAL;
     const bool need_coef = ph & (PH_EVAL | PH_COMPOSITE);
     const bool refr = GEN && do_eval && (flags & WOIT_REFRACTION);
+    const bool diffuse = GEN && (flags & WOIT_DIFFUSION);
     const bool cube = GEN && (flags & WOIT_CUBE_TRANSMISSION);
     const bool bfonly = cube && (flags & WOIT_CUBE_BACKFACE_ONLY);
     const bool need_ior = do_at && (cube || refr);
@@ -702,7 +703,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
         if (do_eval) {
             if (lane < C) {
                 const float2* cq2 = sm.cells + cq * CellRow<M>::CR;
-                float ac[3] = {0.f, 0.f, 0.f}, wg[3] = {0.f, 0.f, 0.f};
+                float ac[3] = {0.f, 0.f, 0.f}, wg[3] = {0.f, 0.f, 0.f}, df = 0.f;
                 double ro[2] = {0.0, 0.0};
                 double d[3] = {0.0, 0.0, 0.0}, topq = INFINITY;
                 const int64_t p = w0 + q0 + cq;
@@ -731,6 +732,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
                         io = sm.ior[si];
                         cb_ = cube && io > 1.0f && (!bfonly || sm.bf[shb + fr] != 0);
                     }
+                    float vs = 0.0f;
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) {
                         // A = lerp of the two neighbouring cell centres, clamped >= 0 (wavelet.py:316-319)
@@ -741,8 +743,10 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
                         const float op = op_staged ? sm.trans[3 * si + ch] : opacity_ch(al, sm.trans[3 * si + ch], cb_);
                         ac[ch] += (Lr * al) * vh;
                         wg[ch] += op * vh;
+                        vs += vh;
                         sm.rad[3 * si + ch] = vh;  // v̂ replaces radiance in place
                     }
+                    if (diffuse) df += al * vs;  // diffusion coverage (woit.h WOIT_DIFFUSION)
                     if (refr && io > 1.0f) {
                         const float nrm[3] = {sm.normal[3 * si], sm.normal[3 * si + 1], sm.normal[3 * si + 2]};
                         double off[2];
@@ -759,6 +763,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
                 }
                 sm.accp[6 * WC + lane] = (float)ro[0];
                 sm.accp[7 * WC + lane] = (float)ro[1];
+                if (GEN) sm.accp[8 * WC + lane] = df;
             }
             fence_proxy_async();  // v̂ in smem becomes visible to the bulk store
             __syncwarp();
@@ -821,8 +826,9 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
         } else if (lane < nqs) {
             const int q = q0 + lane;
             const int64_t p = w0 + q;
-            double acc[3] = {0, 0, 0}, wgt[3] = {0, 0, 0}, ro[2] = {0, 0};
+            double acc[3] = {0, 0, 0}, wgt[3] = {0, 0, 0}, ro[2] = {0, 0}, dsum = 0.0, dp = 0.0;
             const bool acc_in = GEN && ((ph & PH_EVAL_ACC) || ((ph & PH_COMPOSITE) && !do_eval));
+            if (acc_in && diffuse && kp.b.diffusion) dp = kp.b.diffusion[p];
             if (acc_in) {
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) {
@@ -848,6 +854,11 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
                         ro[0] += (double)sm.accp[6 * WC + cc];
                         ro[1] += (double)sm.accp[7 * WC + cc];
                     }
+                    if (diffuse) dsum += (double)sm.accp[8 * WC + cc];
+                }
+                if (diffuse) {
+                    dp = dadd(dp, ddiv(dsum, 3.0));
+                    if (kp.b.diffusion) kp.b.diffusion[p] = (float)dp;
                 }
                 if (kp.b.accum)
                     for (int ch = 0; ch < 3; ++ch) kp.b.accum[p * 3 + ch] = (float)acc[ch];
@@ -861,7 +872,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
             if ((ph & PH_COMPOSITE) && kp.b.output) {
                 float out[3];
                 if (GEN) {
-                    composite_pixel(kp, p, acc, wgt, ro[0], ro[1], sm.vtot + 3 * lane, out);
+                    composite_pixel(kp, p, acc, wgt, ro[0], ro[1], sm.vtot + 3 * lane, dp, out);
                 } else {
                     const int si = (int)(p - ((w0 + q0) & ~(int64_t)3));
                     const float bgc[3] = {sm.opq[3 * si], sm.opq[3 * si + 1], sm.opq[3 * si + 2]};
@@ -893,7 +904,7 @@ __global__ void __launch_bounds__(kLongT) long_pixel_kernel(const KParams kp) {
     double* acc64 = reinterpret_cast<double*>(smem_raw);      // [V][TL]
     double* coef = acc64 + V * TL;                              // [V]
     float* cells = reinterpret_cast<float*>(coef + V);          // [V]
-    __shared__ double red[8][kLongT];
+    __shared__ double red[9][kLongT];
     __shared__ double vt[3];
     __shared__ float nf_s, ff_s;
     const int tid = threadIdx.x;
@@ -1005,7 +1016,7 @@ __global__ void __launch_bounds__(kLongT) long_pixel_kernel(const KParams kp) {
         }
         __syncthreads();
         // eval
-        double lac[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        double lac[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
         if (ph & PH_EVAL) {
             double d[3] = {0, 0, 0}, topq = INFINITY;
             if (refr) {
@@ -1020,13 +1031,16 @@ __global__ void __launch_bounds__(kLongT) long_pixel_kernel(const KParams kp) {
                 const float al = kp.f.alpha[f];
                 const float io = kp.f.ior ? kp.f.ior[f] : 1.0f;
                 const bool cb_ = cube && io > 1.0f && (!bfonly || (kp.f.backface && kp.f.backface[f]));
+                float vs = 0.0f;
                 for (int ch = 0; ch < 3; ++ch) {
                     const float A = fmaxf((1.0f - t) * cells[c0 * 3 + ch] + t * cells[c1 * 3 + ch], 0.0f);
                     const float vh = expf(-A);
                     lac[ch] += (double)((kp.f.radiance[3 * f + ch] * al) * vh);
                     lac[3 + ch] += (double)(opacity_ch(al, kp.f.trans[3 * f + ch], cb_) * vh);
+                    vs += vh;
                     if (kp.b.vhat) kp.b.vhat[3 * f + ch] = vh;
                 }
+                lac[8] += (double)(al * vs);
                 if (refr && io > 1.0f) {
                     const float nrm[3] = {kp.f.normal[3 * f], kp.f.normal[3 * f + 1], kp.f.normal[3 * f + 2]};
                     double off[2];
@@ -1036,11 +1050,11 @@ __global__ void __launch_bounds__(kLongT) long_pixel_kernel(const KParams kp) {
                 }
             }
         }
-        for (int k = 0; k < 8; ++k) red[k][tid] = lac[k];
+        for (int k = 0; k < 9; ++k) red[k][tid] = lac[k];
         __syncthreads();
         for (int o = kLongT / 2; o > 0; o >>= 1) {
             if (tid < o)
-                for (int k = 0; k < 8; ++k) red[k][tid] += red[k][tid + o];
+                for (int k = 0; k < 9; ++k) red[k][tid] += red[k][tid + o];
             __syncthreads();
         }
         if (tid == 0) {
@@ -1053,7 +1067,10 @@ __global__ void __launch_bounds__(kLongT) long_pixel_kernel(const KParams kp) {
             for (int k = 0; k < 2; ++k)
                 ro[k] = (acc_in && kp.b.refraction_offset ? (double)kp.b.refraction_offset[p * 2 + k] : 0.0) +
                         ((ph & PH_EVAL) ? red[6 + k][0] : 0.0);
+            double dp = (acc_in && kp.b.diffusion) ? (double)kp.b.diffusion[p] : 0.0;
+            if (ph & PH_EVAL) dp = dadd(dp, ddiv(red[8][0], 3.0));
             if (ph & PH_EVAL) {
+                if (kp.b.diffusion && (kp.p.flags & WOIT_DIFFUSION)) kp.b.diffusion[p] = (float)dp;
                 if (kp.b.accum)
                     for (int ch = 0; ch < 3; ++ch) kp.b.accum[p * 3 + ch] = (float)acc[ch];
                 if (kp.b.weight)
@@ -1065,7 +1082,7 @@ __global__ void __launch_bounds__(kLongT) long_pixel_kernel(const KParams kp) {
             }
             if ((ph & PH_COMPOSITE) && kp.b.output) {
                 float out[3];
-                composite_pixel(kp, p, acc, wgt, ro[0], ro[1], vt, out);
+                composite_pixel(kp, p, acc, wgt, ro[0], ro[1], vt, dp, out);
                 for (int ch = 0; ch < 3; ++ch) kp.b.output[p * 3 + ch] = out[ch];
             }
         }
@@ -1157,8 +1174,9 @@ __global__ void composite_kernel(const KParams kp) {
     }
     const double ox = kp.b.refraction_offset ? kp.b.refraction_offset[2 * p] : 0.0;
     const double oy = kp.b.refraction_offset ? kp.b.refraction_offset[2 * p + 1] : 0.0;
+    const double dp = kp.b.diffusion ? (double)kp.b.diffusion[p] : 0.0;
     float out[3];
-    composite_pixel(kp, p, acc, wgt, ox, oy, vt, out);
+    composite_pixel(kp, p, acc, wgt, ox, oy, vt, dp, out);
     for (int ch = 0; ch < 3; ++ch) kp.b.output[p * 3 + ch] = out[ch];
 }
 

@@ -90,10 +90,10 @@ WOIT_HD WLayout make_wlayout(uint32_t phases, int flags) {
     L.zfix = o;  o = align16(o + (at ? 4u * G::FBW : 0u));
     // one region, reused: chunk partials [M][3][32] (per-cell differences D) during the
     // build, then the sub-tile's coefficients [SUBP][V], cell staircase [SUBP][VR]
-    // and chunk accumulators [8][32]
+    // and chunk accumulators [9][32]
     const uint32_t part_b = (phases & PH_BUILD) ? 4u * G::V * 32 : 0u;
     const uint32_t CR = 3u * G::S + ((3u + 16u * 64u - 3u * G::S) % 16u);  // frame.cu CellRow
-    const uint32_t after_b = align16(4u * G::SUBP * G::V) + align16(8u * G::SUBP * CR) + (ev ? 4u * 8 * 32 : 0u);
+    const uint32_t after_b = align16(4u * G::SUBP * G::V) + align16(8u * G::SUBP * CR) + (ev ? 4u * 9 * 32 : 0u);
     L.part = o;  o = align16(o + (part_b > after_b ? part_b : after_b));
     L.coef32 = L.part;
     L.cells = L.part + align16(4u * G::SUBP * G::V);
@@ -145,32 +145,20 @@ WOIT_D void bilinear(const float* __restrict__ img, int W, int H, double x, doub
     }
 }
 
-// step4_composite for pixel p (band-local). accum/weight/refr are the pixel's
-// final accumulators, vtot = exp(-A_total).
-WOIT_D void composite_pixel(const KParams& kp, int64_t p, const double acc[3],
-                            const double wgt[3], double ox, double oy, const double vtot[3],
-                            float out[3]) {
-    const int W = kp.f.width;
-    const int flags = kp.p.flags;
-    double bg[3];
+// Background of one pixel read from `img` (pipeline.py:290-303): the k-tap aberration
+// gather, a bilinear sample at the refracted position, or the pixel itself. `img` is
+// [H][W][3] addressed by the pixel id gp (global with a full image, else band-local).
+WOIT_D void sample_background(const float* img, int W, int H, int64_t gp, int flags, int taps,
+                              double ox, double oy, double bg[3]) {
     if (flags & (WOIT_CHROMATIC_ABERRATION | WOIT_REFRACTION)) {
-        const float* img = kp.b.full_opaque_image;
-        int H = kp.f.height;
-        int64_t gp = kp.f.pixel_base + p;
-        if (img == nullptr) {  // band-local image, as step4 without full_opaque_image
-            img = kp.f.opaque_color;
-            H = (int)(kp.f.npix / W);
-            gp = p;
-        }
         const double px = (double)(gp % W), py = (double)(gp / W);
         if (flags & WOIT_CHROMATIC_ABERRATION) {
-            const int k = kp.p.aberration_taps;
             const bool lit = flags & WOIT_LITERAL_SPECTRAL_T;
             double num[3] = {0.0, 0.0, 0.0}, den[3] = {0.0, 0.0, 0.0};
-            for (int i = 0; i < k; ++i) {
+            for (int i = 0; i < taps; ++i) {
                 double w[3], s[3];
-                spectral_weight(i, k, lit, w);
-                const double fac = 2.0 * i / (double)(k - 1);
+                spectral_weight(i, taps, lit, w);
+                const double fac = 2.0 * i / (double)(taps - 1);
                 bilinear(img, W, H, dadd(px, dmul(ox, fac)), dadd(py, dmul(oy, fac)), s);
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) {
@@ -187,7 +175,43 @@ WOIT_D void composite_pixel(const KParams& kp, int64_t p, const double acc[3],
         }
     } else {
 #pragma unroll
+        for (int ch = 0; ch < 3; ++ch) bg[ch] = (double)img[gp * 3 + ch];
+    }
+}
+
+// Diffusion weight w = min(1, diffusion * D_p), D_p = sum alpha (r + g + b) / 3 (woit.h)
+WOIT_D double diffusion_weight(const KParams& kp, double dp) {
+    return fmin(1.0, dmul(kp.p.diffusion, dp));
+}
+
+// step4_composite for pixel p (band-local). accum/weight/refr are the pixel's
+// final accumulators, vtot = exp(-A_total), dp the diffusion coverage D_p
+// (only read with WOIT_DIFFUSION).
+WOIT_D void composite_pixel(const KParams& kp, int64_t p, const double acc[3],
+                            const double wgt[3], double ox, double oy, const double vtot[3],
+                            double dp, float out[3]) {
+    const int W = kp.f.width;
+    const int flags = kp.p.flags;
+    double bg[3];
+    const bool gather = flags & (WOIT_CHROMATIC_ABERRATION | WOIT_REFRACTION);
+    const bool full = kp.b.full_opaque_image != nullptr;
+    // with a full image pixels are addressed globally; else the band is the image
+    const int H = full ? kp.f.height : (int)(kp.f.npix / W);
+    const int64_t gp = full ? kp.f.pixel_base + p : p;
+    if (gather) {
+        sample_background(full ? kp.b.full_opaque_image : kp.f.opaque_color, W, H, gp, flags,
+                          kp.p.aberration_taps, ox, oy, bg);
+    } else {
+#pragma unroll
         for (int ch = 0; ch < 3; ++ch) bg[ch] = (double)kp.f.opaque_color[p * 3 + ch];
+    }
+    if (flags & WOIT_DIFFUSION) {
+        // K_resolve: lerp towards the same sample of the blurred background
+        double bb[3];
+        sample_background(kp.b.blurred_image, W, H, gp, flags, kp.p.aberration_taps, ox, oy, bb);
+        const double w = diffusion_weight(kp, dp);
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) bg[ch] = dadd(bg[ch], dmul(w, dsub(bb[ch], bg[ch])));
     }
     if (flags & WOIT_NORMALIZE) {
 #pragma unroll

@@ -21,6 +21,9 @@ cudaError_t cells_raw(const double* coeffs, const int64_t* pix, const int64_t* c
 cudaError_t total(const double* coeffs, int64_t npix, int rank, double* out, cudaStream_t st);
 cudaError_t pack(const double* v, int64_t n, uint32_t* words, cudaStream_t st);
 cudaError_t unpack(const uint32_t* words, int64_t n, double* out, cudaStream_t st);
+size_t blur_workspace(int32_t width, int32_t height);
+cudaError_t resolve_blur(const float* image, int32_t W, int32_t H, int32_t r, float* out, void* ws,
+                         cudaStream_t st);
 namespace synth {
 struct Out {
     float *depth, *alpha, *trans, *rad, *normal, *ior;

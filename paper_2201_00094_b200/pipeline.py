@@ -14,7 +14,11 @@ Differences from the reference, all deliberate:
 * ``render_frame`` needs ``frame=``: the analytic caster (scene.py:463-630) is
   out of scope, so there is no scene -> fragments step here;
 * only ``method="wavelet"`` renders; the A-buffer / WBOIT / MLAB baselines are
-  out of scope and raise NotImplementedError.
+  out of scope (SURVEY.md §2 row 9) and raise NotImplementedError;
+* ``diffusion`` / ``diffusion_radius`` (default off) add the north star's
+  "resolve and blur" pass, which the reference does not have (SURVEY.md §8 row
+  GAP): an in-repo definition, documented in include/woit.h (WOIT_DIFFUSION) and
+  DESIGN.md, parity unpinned. With diffusion == 0 nothing changes.
 """
 
 from __future__ import annotations
@@ -52,6 +56,8 @@ class RenderConfig:
     literal_spectral_t: bool = False
     cube_backface_only: bool = False
     wboit_weight: Tuple[float, float, float] = DEFAULT_WBOIT_WEIGHT
+    diffusion: float = 0.0        # in-repo "resolve and blur" strength (0 = off)
+    diffusion_radius: int = 4     # Gaussian taps each side, sigma = radius / 2
 
     def __post_init__(self):
         if self.method not in METHODS:
@@ -64,6 +70,10 @@ class RenderConfig:
             raise ValueError("frame must be at least 1x1")
         if self.workers < 1:
             raise ValueError("workers must be >= 1")
+        if not (math.isfinite(self.diffusion) and self.diffusion >= 0.0):
+            raise ValueError("diffusion must be finite and >= 0")
+        if not (1 <= self.diffusion_radius <= 64):
+            raise ValueError("diffusion_radius must lie in [1, 64]")
 
     @property
     def flags(self) -> int:
@@ -75,6 +85,7 @@ class RenderConfig:
         f |= _lib.PACKED_STORAGE if self.packed_storage else 0
         f |= _lib.LITERAL_SPECTRAL_T if self.literal_spectral_t else 0
         f |= _lib.CUBE_BACKFACE_ONLY if self.cube_backface_only else 0
+        f |= _lib.DIFFUSION if self.diffusion > 0.0 else 0
         return f
 
 
@@ -146,6 +157,7 @@ class FrameBuffers:
     opaque_color: torch.Tensor
     output: torch.Tensor
     vhat: Optional[torch.Tensor] = None  # per-fragment transmittance (filled by step3 / render)
+    diffusion: Optional[torch.Tensor] = None  # per-pixel coverage D_p (WOIT_DIFFUSION)
 
     @classmethod
     def allocate(cls, frame: FrameFragments, rank: int, vhat: bool = False) -> "FrameBuffers":
@@ -156,12 +168,13 @@ class FrameBuffers:
                    torch.full((P,), -math.inf, dtype=torch.float32, device=dev),
                    z(P, 1 << (rank + 1), 3), z(P, 3), z(P, 3), z(P, 2),
                    frame.opaque_depth.clone(), frame.opaque_color.clone(), z(P, 3),
-                   z(frame.nfrag, 3) if vhat else None)
+                   z(frame.nfrag, 3) if vhat else None, z(P))
 
     def image(self) -> torch.Tensor:
         return self.output.reshape(-1, self.width, 3)
 
-    def c_struct(self, full_opaque_image: Optional[torch.Tensor] = None) -> _lib.Bufs:
+    def c_struct(self, full_opaque_image: Optional[torch.Tensor] = None,
+                 blurred_image: Optional[torch.Tensor] = None) -> _lib.Bufs:
         b = _lib.Bufs()
         b.near, b.far, b.coeffs = ptr(self.near), ptr(self.far), ptr(self.coeffs)
         b.accum, b.weight = ptr(self.accum), ptr(self.accum_weight)
@@ -171,6 +184,11 @@ class FrameBuffers:
             full_opaque_image = full_opaque_image.to(torch.float32).contiguous()
             self._img_keepalive = full_opaque_image
         b.full_opaque_image = ptr(full_opaque_image)
+        b.diffusion = ptr(self.diffusion)
+        if blurred_image is not None:
+            blurred_image = blurred_image.to(torch.float32).contiguous()
+            self._blur_keepalive = blurred_image
+        b.blurred_image = ptr(blurred_image)
         return b
 
 
@@ -185,6 +203,7 @@ def _params(cfg: RenderConfig, rank: int, rays: Optional[RayGrid] = None) -> _li
         p.cam_right[i] = float(rays.right[i])
         p.cam_up[i] = float(rays.up[i])
     p.tan_half, p.aspect = float(rays.tan_half), float(rays.aspect)
+    p.diffusion, p.diffusion_radius = float(cfg.diffusion), int(cfg.diffusion_radius)
     return p
 
 
@@ -273,16 +292,54 @@ def step3_accumulate(rays, frame: FrameFragments, bufs: FrameBuffers, cfg: Rende
         counter.record_eval(2 * frame.nfrag, 2 * frame.nfrag * (bufs.rank + 2))
 
 
+def resolve_blur(image: torch.Tensor, radius: int, ws: Optional[Workspace] = None) -> torch.Tensor:
+    """K_resolve: separable edge-clamped Gaussian blur of an (H, W, 3) fp32 image.
+
+    The in-repo diffusion definition (include/woit.h, WOIT_DIFFUSION); the
+    reference has no such pass (SURVEY.md §8 row GAP), so its parity is unpinned.
+    """
+    if image.dim() != 3 or image.shape[-1] != 3:
+        raise ValueError("image must be (H, W, 3)")
+    if not (1 <= radius <= 64):
+        raise ValueError("diffusion_radius must lie in [1, 64]")
+    lib = _lib.load()
+    img = image.to(torch.float32).contiguous()
+    H, W = int(img.shape[0]), int(img.shape[1])
+    out = torch.empty_like(img)
+    n = lib.woit_blur_workspace_bytes(W, H)
+    t = (ws or _BLUR_WS).get(n, img.device)
+    _lib.check(lib.woit_resolve_blur(ptr(img), W, H, int(radius), ptr(out), ptr(t), t.numel(), _stream()),
+               "resolve_blur")
+    return out
+
+
+_BLUR_WS = Workspace()
+
+
+def _background_image(bufs_or_frame, full_opaque_image: Optional[torch.Tensor]) -> torch.Tensor:
+    """The image the background is read from: the full frame, else the band itself."""
+    if full_opaque_image is not None:
+        return full_opaque_image
+    return bufs_or_frame.opaque_color.reshape(-1, bufs_or_frame.width, 3)
+
+
 def step4_composite(bufs: FrameBuffers, cfg: RenderConfig, counter: Optional[TouchCounter] = None,
-                    pixel_base: int = 0, full_opaque_image: Optional[torch.Tensor] = None) -> None:
-    """Blend over the (refracted / aberrated) background (pipeline.py:284-308)."""
+                    pixel_base: int = 0, full_opaque_image: Optional[torch.Tensor] = None,
+                    blurred_image: Optional[torch.Tensor] = None) -> None:
+    """Blend over the (refracted / aberrated) background (pipeline.py:284-308).
+
+    With ``cfg.diffusion > 0`` the background is lerped towards ``blurred_image``
+    (computed here by ``resolve_blur`` when not given) by min(1, diffusion * D_p).
+    """
     lib = _lib.load()
     P = bufs.near.numel()
     f = _lib.Frags()
     f.width, f.height = bufs.width, bufs.height
     f.npix, f.pixel_base = P, pixel_base
     f.opaque_color = ptr(bufs.opaque_color)
-    b = bufs.c_struct(full_opaque_image)
+    if cfg.diffusion > 0.0 and blurred_image is None:
+        blurred_image = resolve_blur(_background_image(bufs, full_opaque_image), cfg.diffusion_radius)
+    b = bufs.c_struct(full_opaque_image, blurred_image)
     _lib.check(lib.woit_step4_composite(f, _params(cfg, bufs.rank), b, _stream()), "step4_composite")
     if counter is not None:
         counter.record_eval(P, P * (bufs.rank + 2))
@@ -291,13 +348,19 @@ def step4_composite(bufs: FrameBuffers, cfg: RenderConfig, counter: Optional[Tou
 def render_band(frame: FrameFragments, cfg: RenderConfig, rays: Optional[RayGrid] = None,
                 bufs: Optional[FrameBuffers] = None, full_opaque_image: Optional[torch.Tensor] = None,
                 vhat: bool = False, counter: Optional[TouchCounter] = None,
-                ws: Optional[Workspace] = None) -> FrameBuffers:
-    """All four passes fused in one kernel (pipeline.py:321-330, _wavelet_band)."""
+                ws: Optional[Workspace] = None, blurred_image: Optional[torch.Tensor] = None) -> FrameBuffers:
+    """All four passes fused in one kernel (pipeline.py:321-330, _wavelet_band).
+
+    With ``cfg.diffusion > 0`` the K_resolve blur of the background image runs
+    first (``resolve_blur``; pass ``blurred_image`` to reuse one across bands).
+    """
     lib = _lib.load()
     if bufs is None:
         bufs = FrameBuffers.allocate(frame, cfg.rank, vhat=vhat)
     _check_frame(frame, bufs)
-    f, b = frame.c_struct(), bufs.c_struct(full_opaque_image)
+    if cfg.diffusion > 0.0 and blurred_image is None:
+        blurred_image = resolve_blur(_background_image(frame, full_opaque_image), cfg.diffusion_radius)
+    f, b = frame.c_struct(), bufs.c_struct(full_opaque_image, blurred_image)
     w, wn = _frame_ws(frame, ws)
     _lib.check(lib.woit_render_band(f, _params(cfg, bufs.rank, rays), b, w, wn, _stream()),
                "render_band")
@@ -327,8 +390,9 @@ def render_frame(scene, cfg: RenderConfig, counter: Optional[TouchCounter] = Non
     cam = getattr(scene, "camera", scene) if scene is not None else None
     rays = camera_rays(cam if isinstance(cam, Camera) else _as_camera(cam), cfg.width, cfg.height)
     full_img = frame.opaque_color.reshape(cfg.height, cfg.width, 3)
+    blurred = resolve_blur(full_img, cfg.diffusion_radius) if cfg.diffusion > 0.0 else None
     if cfg.workers == 1 or cfg.height < 2 * cfg.workers:
-        bufs = render_band(frame, cfg, rays, full_opaque_image=full_img, counter=counter)
+        bufs = render_band(frame, cfg, rays, full_opaque_image=full_img, counter=counter, blurred_image=blurred)
         return bufs.output.reshape(cfg.height, cfg.width, 3)
     rows = [int(r) for r in torch.linspace(0, cfg.height, cfg.workers + 1).to(torch.int64)]
     out = torch.empty(frame.npix, 3, dtype=torch.float32, device=frame.device)
@@ -337,7 +401,7 @@ def render_frame(scene, cfg: RenderConfig, counter: Optional[TouchCounter] = Non
             continue
         p0, p1 = r0 * cfg.width, r1 * cfg.width
         band = frame.band(p0, p1)
-        bufs = render_band(band, cfg, rays, full_opaque_image=full_img, counter=counter)
+        bufs = render_band(band, cfg, rays, full_opaque_image=full_img, counter=counter, blurred_image=blurred)
         out[p0:p1] = bufs.output
     return out.reshape(cfg.height, cfg.width, 3)
 

@@ -156,6 +156,15 @@ int woit_step3_accumulate(const woit_frags_t* frags, const woit_params_t* params
 int woit_step4_composite(const woit_frags_t* frags, const woit_params_t* params,
                          woit_bufs_t* bufs, void* stream);
 
+/* The north star's alternative build, kept for the measured comparison (DESIGN.md
+ * §3.6): step2_build on an UNBINNED stream with explicit pixel ids pix[nfrag]
+ * (frags->offsets unused), one thread per fragment scattering the closed-form
+ * projection (wavelet.py:272-287) with fp32 red.global.add into coeffs (which the
+ * caller zeroes). Not bit-reproducible (atomic order); no packed storage. */
+size_t woit_build_atomic_workspace_bytes(int64_t npix);
+int woit_build_atomic(const woit_frags_t* frags, const int32_t* pix, const woit_params_t* params,
+                      woit_bufs_t* bufs, void* ws, size_t ws_bytes, void* stream);
+
 /* Per-fragment normalised depth z (double[n]), level slot offsets k_n
  * (int32[n][rank+1], wavelet.py:281) and interpolation cells c0, c1
  * (int32[n][2], wavelet.py:309-315), computed by the same device functions the

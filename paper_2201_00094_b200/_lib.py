@@ -75,6 +75,8 @@ _SIGS = {
     "woit_step4_composite": (C.c_int, [C.POINTER(Frags), C.POINTER(Params), C.POINTER(Bufs), _vp]),
     "woit_fragment_indices": (C.c_int, [C.POINTER(Frags), _vp, _vp, C.c_int, _vp, _vp, _vp, _vp]),
     "woit_blur_workspace_bytes": (_sz, [_i32, _i32]),
+    "woit_build_atomic_workspace_bytes": (_sz, [_i64]),
+    "woit_build_atomic": (C.c_int, [C.POINTER(Frags), _vp, C.POINTER(Params), C.POINTER(Bufs), _vp, _sz, _vp]),
     "woit_resolve_blur": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _vp, _sz, _vp]),
     "woit_build_into_workspace_bytes": (_sz, [_i64, _i64]),
     "woit_build_into": (C.c_int, [_vp, _i64, _vp, _vp, _vp, _i64, C.c_int, C.c_int, _vp, _sz, _vp]),

@@ -172,6 +172,22 @@ int woit_fragment_indices(const woit_frags_t* frags, const float* near, const fl
     return cuda_status(launch_indices(kp, z, slots, cells, static_cast<cudaStream_t>(stream)));
 }
 
+size_t woit_build_atomic_workspace_bytes(int64_t npix) { return npix < 0 ? 0 : build_atomic_workspace(npix); }
+
+int woit_build_atomic(const woit_frags_t* frags, const int32_t* pix, const woit_params_t* params, woit_bufs_t* bufs,
+                      void* ws, size_t ws_bytes, void* stream) {
+    int s = check_params(params);
+    if (s) return s;
+    if (!frags || frags->npix < 0 || frags->nfrag < 0 || !bufs) return WOIT_EINVAL;
+    if (params->flags & WOIT_PACKED_STORAGE) return WOIT_EINVAL;
+    if (!bufs->near || !bufs->far || !bufs->coeffs) return WOIT_EINVAL;
+    if (frags->nfrag > 0 && (!pix || !frags->depth || !frags->alpha || !frags->trans)) return WOIT_EINVAL;
+    if (frags->npix == 0) return WOIT_OK;
+    if (!ws || ws_bytes < build_atomic_workspace(frags->npix)) return WOIT_EWORKSPACE;
+    return cuda_status(build_atomic(pix, *frags, params->rank, params->flags, bufs->near, bufs->far, bufs->coeffs, ws,
+                                    static_cast<cudaStream_t>(stream)));
+}
+
 size_t woit_blur_workspace_bytes(int32_t width, int32_t height) {
     return width < 1 || height < 1 ? 0 : blur_workspace(width, height);
 }

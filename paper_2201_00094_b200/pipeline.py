@@ -272,6 +272,35 @@ def step2_build(frame: FrameFragments, bufs: FrameBuffers, cfg: RenderConfig,
         counter.record_insert(frame.nfrag, frame.nfrag * (bufs.rank + 2))
 
 
+def pixel_ids(frame: FrameFragments) -> torch.Tensor:
+    """int32 pixel id per fragment (the reference's FrameFragments.pixel, scene.py:369)."""
+    run = frame.offsets[1:] - frame.offsets[:-1]
+    return torch.repeat_interleave(torch.arange(frame.npix, device=frame.device, dtype=torch.int32), run)
+
+
+def step2_build_atomic(frame: FrameFragments, bufs: FrameBuffers, cfg: RenderConfig,
+                       pix: Optional[torch.Tensor] = None, ws: Optional[Workspace] = None) -> None:
+    """step2_build through the north star's alternative: fp32 red.global atomics of the
+    closed-form projection from an unbinned stream (``pix`` = pixel id per fragment).
+
+    Kept for the measured comparison against the CSR tile build (DESIGN.md §3.6);
+    not bit-reproducible run to run. ``bufs.coeffs`` is accumulated into.
+    """
+    _check_frame(frame, bufs)
+    if cfg.packed_storage:
+        raise ValueError("the atomic build has no packed storage")
+    lib = _lib.load()
+    if pix is None:
+        pix = pixel_ids(frame)
+    if pix.dtype != torch.int32 or pix.numel() < frame.nfrag:
+        raise ValueError("pix must be int32 with one id per fragment")
+    n = lib.woit_build_atomic_workspace_bytes(frame.npix)
+    t = (ws or _WS).get(n, frame.device)
+    f, b = frame.c_struct(), bufs.c_struct()
+    _lib.check(lib.woit_build_atomic(f, ptr(pix), _params(cfg, bufs.rank), b, ptr(t), t.numel(), _stream()),
+               "step2_build_atomic")
+
+
 def step3_accumulate(rays, frame: FrameFragments, bufs: FrameBuffers, cfg: RenderConfig,
                      counter: Optional[TouchCounter] = None, pixel_base: int = 0,
                      ws: Optional[Workspace] = None) -> None:

@@ -17,6 +17,9 @@
 #ifndef WOIT_ZUNROLL
 #define WOIT_ZUNROLL 8
 #endif
+#ifndef WOIT_FFMA2
+#define WOIT_FFMA2 1
+#endif
 #ifndef WOIT_PERSIST  // resident CTAs per SM slot multiplier for the persistent grid (0: one CTA per 2 windows)
 #define WOIT_PERSIST 1
 #endif
@@ -147,12 +150,30 @@ WOIT_D void build_chunk_fast(const zfix_t* __restrict__ zf, const float* __restr
         const zfix_t zi = zf[fr];
         const float al = alp[si];
         float a[3];
+#if WOIT_FFMA2
+        {   // channels 0 and 1 paired (bit-identical to the scalar sequence), channel 2 scalar
+            const float2 one = make_float2(1.0f, 1.0f);
+            const float2 T01 = make_float2(trs[3 * si], trs[3 * si + 1]);
+            const float2 op01 = __fmul2_rn(make_float2(al, al), __fadd2_rn(one, make_float2(-T01.x, -T01.y)));
+            const float op2 = opacity_ch(al, trs[3 * si + 2], false);
+            trs[3 * si] = op01.x;  // the evaluation's weight 1 - t (pipeline.py:184)
+            trs[3 * si + 1] = op01.y;
+            trs[3 * si + 2] = op2;
+            const float2 y01 = __fadd2_rn(one, make_float2(-op01.x, -op01.y));
+            const float2 l01 = log_poly2(make_float2(fmaxf((float)kTransFloor, y01.x),
+                                                     fmaxf((float)kTransFloor, y01.y)));
+            a[0] = -l01.x;
+            a[1] = -l01.y;
+            a[2] = -log_poly(fmaxf((float)kTransFloor, 1.0f - op2));
+        }
+#else
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
             const float op = opacity_ch(al, trs[3 * si + ch], false);
             trs[3 * si + ch] = op;  // the evaluation's weight 1 - t (pipeline.py:184)
             a[ch] = -log_poly(fmaxf((float)kTransFloor, 1.0f - op));
         }
+#endif
         const int cell = (int)(zi >> (kZBits - (R + 1)));
         const float fr_ = u32_to_unit(zi << (R + 1), kZBits);  // M z - j_f
         float* d = part + cell * 3 * WC + lane;

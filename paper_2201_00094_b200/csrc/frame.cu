@@ -12,10 +12,13 @@
 #include "frame.cuh"
 
 #ifndef WOIT_UNROLL
-#define WOIT_UNROLL 2
+#define WOIT_UNROLL 1
 #endif
 #ifndef WOIT_ZUNROLL
 #define WOIT_ZUNROLL 8
+#endif
+#ifndef WOIT_FUSEZ  // fast path: z computed inside the build loop
+#define WOIT_FUSEZ 1
 #endif
 #ifndef WOIT_FFMA2
 #define WOIT_FFMA2 1
@@ -137,10 +140,16 @@ WOIT_D void store_cells(float2* cells, int kq, int kch, const TV v[M]) {
 // then move the loads of later fragments above the shared-memory stores of earlier
 // ones (the pointers provably do not alias), which it cannot do in the kernel body.
 template <int R>
-WOIT_D void build_frag(const zfix_t* __restrict__ zf, const float* __restrict__ alp, float* __restrict__ trs,
-                       float* __restrict__ part, float* __restrict__ sink, int lane, int fr, int si) {
+WOIT_D void build_frag(zfix_t* __restrict__ zf, const float* __restrict__ dep, const DepthMap& m,
+                       const float* __restrict__ alp, float* __restrict__ trs, float* __restrict__ part,
+                       float* __restrict__ sink, int lane, int fr, int si) {
     constexpr int M = 2 << R, WC = 32;
+#if WOIT_FUSEZ
+    const zfix_t zi = z_fixed_of(dep[si], m);  // z fused into the build; kept for the evaluation
+    zf[fr] = zi;
+#else
     const zfix_t zi = zf[fr];
+#endif
     const float al = alp[si];
     float a[3];
 #if WOIT_FFMA2
@@ -182,15 +191,15 @@ WOIT_D void build_frag(const zfix_t* __restrict__ zf, const float* __restrict__ 
 // The chunk loops visit fragment (crot + j) mod clen at step j. (Fully unrolled
 // loops for full chunks measured 3.5% slower: code size.)
 template <int R>
-WOIT_D void build_chunk_fast(const zfix_t* __restrict__ zf, const float* __restrict__ alp,
-                             float* __restrict__ trs, float* __restrict__ part, float* __restrict__ sink,
-                             int lane, int cst, int clen, int crot, int sh4) {
+WOIT_D void build_chunk_fast(zfix_t* __restrict__ zf, const float* __restrict__ dep, const DepthMap m,
+                             const float* __restrict__ alp, float* __restrict__ trs, float* __restrict__ part,
+                             float* __restrict__ sink, int lane, int cst, int clen, int crot, int sh4) {
     int jj = crot;
 #pragma unroll kUnroll
     for (int j = 0; j < clen; ++j) {
         const int fr = cst + jj;
         jj = jj + 1 == clen ? 0 : jj + 1;
-        build_frag<R>(zf, alp, trs, part, sink, lane, fr, sh4 + fr);
+        build_frag<R>(zf, dep, m, alp, trs, part, sink, lane, fr, sh4 + fr);
     }
 }
 
@@ -529,7 +538,8 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
 
         // ---- 4. z (fixed point) and build (step2): chunk partials -> part[v][lane] ----
         float* part = sm.part;
-        if (lane < C && do_at) {
+        const bool fused_z = !GEN && WOIT_FUSEZ && (ph & PH_BUILD);  // the fast build computes z itself
+        if (lane < C && do_at && !fused_z) {
             const DepthMap m{sm.lo[cq], sm.den[cq], 0.0, sm.rcp[cq]};
 #pragma unroll kZUnroll
             for (int j = 0; j < CH; ++j) {  // independent chains: unrolled for ILP
@@ -558,7 +568,8 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
             // scratch [3][32] for the dropped D_M terms: vtot is dead until phase 5
             float* sink = reinterpret_cast<float*>(sm.vtot) + lane;
             if (!GEN && lane < C) {
-                build_chunk_fast<R>(sm.zfix, sm.alpha, sm.trans, part, sink, lane, cst, clen, crot, sh4);
+                build_chunk_fast<R>(sm.zfix, sm.depth, DepthMap{sm.lo[cq], sm.den[cq], 0.0, sm.rcp[cq]}, sm.alpha,
+                                    sm.trans, part, sink, lane, cst, clen, crot, sh4);
             } else if (lane < C) {
                 int jj = crot;
 #pragma unroll kUnroll

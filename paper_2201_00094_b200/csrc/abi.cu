@@ -61,10 +61,11 @@ int run_frame(const woit_frags_t* f, const woit_params_t* p, woit_bufs_t* b, uin
     bool al = true;
     for (const void* q : ptrs) al = al && (q == nullptr || aligned16(q));
     kp.use_tma = al ? 1 : 0;
-    kp.long_list = static_cast<int64_t*>(ws);
+    kp.win_counter = static_cast<unsigned long long*>(ws);
+    kp.long_list = static_cast<int64_t*>(ws) + 1;
     kp.long_cap = long_cap(f->nfrag);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    cudaError_t err = cudaMemsetAsync(ws, 0, sizeof(int64_t), st);
+    cudaError_t err = cudaMemsetAsync(ws, 0, 2 * sizeof(int64_t), st);
     if (err != cudaSuccess) return WOIT_ECUDA;
     return cuda_status(launch_frame(kp, st));
 }
@@ -89,7 +90,7 @@ const char* woit_status_string(int status) {
 
 size_t woit_frame_workspace_bytes(int64_t npix, int64_t nfrag) {
     (void)npix;
-    return (size_t)(1 + long_cap(nfrag)) * sizeof(int64_t);
+    return (size_t)(2 + long_cap(nfrag)) * sizeof(int64_t);  // window counter, long count, long list
 }
 
 int woit_render_band(const woit_frags_t* frags, const woit_params_t* params, woit_bufs_t* bufs, void* ws,
@@ -156,6 +157,7 @@ int woit_step4_composite(const woit_frags_t* frags, const woit_params_t* params,
     kp.use_tma = 0;
     kp.long_list = nullptr;
     kp.long_cap = 0;
+    kp.win_counter = nullptr;
     return cuda_status(launch_composite(kp, static_cast<cudaStream_t>(stream)));
 }
 

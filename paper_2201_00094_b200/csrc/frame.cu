@@ -17,8 +17,19 @@
 #ifndef WOIT_ZUNROLL
 #define WOIT_ZUNROLL 8
 #endif
-#ifndef WOIT_FUSEZ  // fast path: z computed inside the build loop
-#define WOIT_FUSEZ 1
+#ifndef WOIT_ALIASZ  // fast path: fixed-point z stored over the staged depth
+#define WOIT_ALIASZ 1
+#endif
+#ifndef WOIT_ZR_ON
+#define WOIT_ZR_ON 1
+#endif
+#if WOIT_ZR_ON
+#define WOIT_ZR __restrict__
+#else
+#define WOIT_ZR
+#endif
+#ifndef WOIT_DYN  // dynamic window claims
+#define WOIT_DYN 1
 #endif
 #ifndef WOIT_FFMA2
 #define WOIT_FFMA2 1
@@ -49,10 +60,6 @@ WOIT_D void unpack_chunk(uint32_t c, int& q, int& start, int& len) {
 // of the tiling (bit-identical results for any band split).
 WOIT_D int chunk_rotation(int64_t gstart, int len) { return (int)((uint32_t)(gstart >> 5) % (uint32_t)len); }
 
-// rotation of the chunk loop in the per-pixel combine (same purpose)
-WOIT_D int combine_rotation(int64_t gpix, int nch) {
-    return (int)((uint32_t)((gpix * nch) >> 5) % (uint32_t)nch);
-}
 
 // ---------------------------------------------------------------------------
 // staging: [fa, fb) of one array into shared memory at index (f - a), where a
@@ -140,16 +147,14 @@ WOIT_D void store_cells(float2* cells, int kq, int kch, const TV v[M]) {
 // then move the loads of later fragments above the shared-memory stores of earlier
 // ones (the pointers provably do not alias), which it cannot do in the kernel body.
 template <int R>
-WOIT_D void build_frag(zfix_t* __restrict__ zf, const float* __restrict__ dep, const DepthMap& m,
+WOIT_D void build_frag(zfix_t* WOIT_ZR zf, const float* WOIT_ZR dep, const DepthMap& m,
                        const float* __restrict__ alp, float* __restrict__ trs, float* __restrict__ part,
                        float* __restrict__ sink, int lane, int fr, int si) {
     constexpr int M = 2 << R, WC = 32;
-#if WOIT_FUSEZ
-    const zfix_t zi = z_fixed_of(dep[si], m);  // z fused into the build; kept for the evaluation
+    // z fused into the build and stored for the evaluation (fast path: in place of
+    // the depth, which nothing reads afterwards)
+    const zfix_t zi = z_fixed_of(dep[si], m);
     zf[fr] = zi;
-#else
-    const zfix_t zi = zf[fr];
-#endif
     const float al = alp[si];
     float a[3];
 #if WOIT_FFMA2
@@ -191,7 +196,7 @@ WOIT_D void build_frag(zfix_t* __restrict__ zf, const float* __restrict__ dep, c
 // The chunk loops visit fragment (crot + j) mod clen at step j. (Fully unrolled
 // loops for full chunks measured 3.5% slower: code size.)
 template <int R>
-WOIT_D void build_chunk_fast(zfix_t* __restrict__ zf, const float* __restrict__ dep, const DepthMap m,
+WOIT_D void build_chunk_fast(zfix_t* WOIT_ZR zf, const float* WOIT_ZR dep, const DepthMap m,
                              const float* __restrict__ alp, float* __restrict__ trs, float* __restrict__ part,
                              float* __restrict__ sink, int lane, int cst, int clen, int crot, int sh4) {
     int jj = crot;
@@ -249,9 +254,7 @@ WOIT_D void eval_chunk_fast(const zfix_t* __restrict__ zf, const float* __restri
 template <int R, bool GEN>
 struct WSmem {
     int64_t* offs;     // [WIN+1] window CSR offsets
-    int32_t* nch;      // [WIN]   chunks per pixel
     int32_t* cb;       // [WIN+1] window chunk prefix
-    int32_t* rot;      // [WIN]   combine rotation
     uint32_t* nearu;   // [WIN]   ordered-int near / far
     uint32_t* faru;
     double* lo;        // [WIN]   depth map
@@ -280,9 +283,7 @@ template <int R, bool GEN>
 WOIT_D WSmem<R, GEN> wcarve(unsigned char* base, const WLayout& L) {
     WSmem<R, GEN> s;
     s.offs = reinterpret_cast<int64_t*>(base + L.offs);
-    s.nch = reinterpret_cast<int32_t*>(base + L.nch);
     s.cb = reinterpret_cast<int32_t*>(base + L.cb);
-    s.rot = reinterpret_cast<int32_t*>(base + L.rot);
     s.nearu = reinterpret_cast<uint32_t*>(base + L.nearu);
     s.faru = reinterpret_cast<uint32_t*>(base + L.faru);
     s.lo = reinterpret_cast<double*>(base + L.lo);
@@ -318,16 +319,27 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const uint32_t ph = GEN ? kp.phases : kFused;
     const int flags = GEN ? kp.p.flags : (kp.p.flags & WOIT_NORMALIZE);
-    const WLayout L = make_wlayout<R>(ph, flags);
+    const WLayout L = make_wlayout<R>(ph, flags, !GEN && WOIT_ALIASZ);
     const int lane = threadIdx.x & 31;
     WSmem<R, GEN> sm = wcarve<R, GEN>(smem_raw + (threadIdx.x >> 5) * L.total, L);
 
-    // persistent warps: window w = warp id + k * (total warps), next window's CSR
-    // offsets prefetched into registers while the current one is processed
+    // persistent warps: the first window is the warp id, later ones are claimed from
+    // a global counter (dynamic: the SM sub-partitions hold unequal warp counts and
+    // windows unequal work). The next window's CSR offsets are prefetched into
+    // registers while the current one is processed.
     const int64_t nwin = (kp.f.npix + WIN - 1) / WIN;
-    const int64_t wstride = (int64_t)gridDim.x * G::WPB;
+    const int64_t nwarps = (int64_t)gridDim.x * G::WPB;
     int64_t win = (int64_t)blockIdx.x * G::WPB + (threadIdx.x >> 5);
     if (win >= nwin) return;  // warp-uniform
+    auto claim = [&]() -> int64_t {
+#if WOIT_DYN
+        unsigned long long c = 0;
+        if (lane == 0) c = atomicAdd(kp.win_counter, 1ull);
+        return nwarps + (int64_t)__shfl_sync(0xffffffffu, c, 0);
+#else
+        return win + nwarps;
+#endif
+    };
 
     const bool do_at = ph & (PH_BUILD | PH_EVAL);
     const bool do_eval = ph & PH_EVAL;
@@ -348,13 +360,15 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
         if (win * WIN + lane < end) off_lane = kp.f.offsets[win * WIN + lane];
         off_last = kp.f.offsets[end];
     }
-    for (; win < nwin; win += wstride) {
+    int64_t next_win = nwin;
+    for (; win < nwin; win = next_win) {
     const int64_t w0 = win * WIN;
     const int nq = (int)((kp.f.npix - w0) < WIN ? (kp.f.npix - w0) : WIN);
     if (lane < nq) sm.offs[lane] = off_lane;
     if (lane == 0) sm.offs[nq] = off_last;
     {   // prefetch the next window's offsets (consumed one window later)
-        const int64_t nw = win + wstride;
+        const int64_t nw = claim();
+        next_win = nw;
         if (nw < nwin) {
             const int64_t nw0 = nw * WIN;
             const int64_t nend = (nw0 + WIN) < kp.f.npix ? (nw0 + WIN) : kp.f.npix;
@@ -369,7 +383,6 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
         const int64_t run = sm.offs[lane + 1] - sm.offs[lane];
         const int64_t nc64 = (run + CH - 1) / CH;
         my_nch = nc64 > (1 << 24) ? (1 << 24) : (int)nc64;  // long pixels never form a sub-tile
-        sm.nch[lane] = my_nch;
     }
     int inc = my_nch;
 #pragma unroll
@@ -481,7 +494,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
         if (lane < nqs) {
             const int q = q0 + lane;
             const int run = (int)(sm.offs[q + 1] - sm.offs[q]);
-            const int nc = sm.nch[q];
+            const int nc = (sm.cb[q + 1] - sm.cb[q]);
             const int base = sm.cb[q] - sm.cb[q0];
             const int rel = (int)(sm.offs[q] - fa);
             // chunk i of the pixel = fragments [CH i, min(CH (i+1), run)): a function of
@@ -538,7 +551,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
 
         // ---- 4. z (fixed point) and build (step2): chunk partials -> part[v][lane] ----
         float* part = sm.part;
-        const bool fused_z = !GEN && WOIT_FUSEZ && (ph & PH_BUILD);  // the fast build computes z itself
+        const bool fused_z = !GEN && (ph & PH_BUILD);  // the fast build computes z itself
         if (lane < C && do_at && !fused_z) {
             const DepthMap m{sm.lo[cq], sm.den[cq], 0.0, sm.rcp[cq]};
 #pragma unroll kZUnroll
@@ -560,16 +573,20 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
         // prefix sum of D. The reference's coefficients are the Haar analysis of v
         // (phase 5) -- its closed form (wavelet.py:272-287) up to rounding.
         if (ph & PH_BUILD) {
+            // this chunk's depth map, read before the sink below reuses its bytes
+            DepthMap mq{0.0, 0.0, 0.0, 0.0};
+            if (!GEN && lane < C) mq = DepthMap{sm.lo[cq], sm.den[cq], 0.0, sm.rcp[cq]};
             {   // zero the partials [M][3][32] cooperatively, 16 B per store
                 float4* pz = reinterpret_cast<float4*>(part);
                 for (int i = lane; i < (M * 3 * WC) / 4; i += 32) pz[i] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
             __syncwarp();
-            // scratch [3][32] for the dropped D_M terms: vtot is dead until phase 5
-            float* sink = reinterpret_cast<float*>(sm.vtot) + lane;
+            // scratch [3][32] for the dropped D_M terms: the depth maps and vtot
+            // (contiguous, >= 384 B) are dead until phase 5 / the next sub-tile
+            float* sink = reinterpret_cast<float*>(sm.lo) + lane;
             if (!GEN && lane < C) {
-                build_chunk_fast<R>(sm.zfix, sm.depth, DepthMap{sm.lo[cq], sm.den[cq], 0.0, sm.rcp[cq]}, sm.alpha,
-                                    sm.trans, part, sink, lane, cst, clen, crot, sh4);
+                build_chunk_fast<R>(sm.zfix + (WOIT_ALIASZ ? sh4 : 0), sm.depth, mq, sm.alpha, sm.trans, part, sink,
+                                    lane, cst, clen, crot, sh4);
             } else if (lane < C) {
                 int jj = crot;
 #pragma unroll kUnroll
@@ -614,7 +631,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
             float rc[M];
             if (task) {
                 const int q = q0 + kq;
-                const int nc = sm.nch[q];
+                const int nc = (sm.cb[q + 1] - sm.cb[q]);
                 const int cbq = sm.cb[q] - sm.cb[q0];
                 const float* pv = part + kch * WC + cbq;
 #pragma unroll
@@ -758,7 +775,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
                 }
                 const bool op_staged = ph & PH_BUILD;  // the build left alpha (1 - T') in the trans slot
                 if (!GEN) {
-                    eval_chunk_fast<R>(sm.zfix, sm.alpha, sm.trans, cq2, sm.rad, cst, clen, crot, sh4, ac, wg);
+                    eval_chunk_fast<R>(sm.zfix + (WOIT_ALIASZ ? sh4 : 0), sm.alpha, sm.trans, cq2, sm.rad, cst, clen, crot, sh4, ac, wg);
                 } else {
                 int jj = crot;
 #pragma unroll kUnroll
@@ -841,7 +858,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
                 const int kch = lane / nqs, kq = lane - kch * nqs;
                 const int q = q0 + kq;
                 const int64_t p = w0 + q;
-                const int nc = sm.nch[q];
+                const int nc = (sm.cb[q + 1] - sm.cb[q]);
                 const int cbq = sm.cb[q] - sm.cb[q0];
                 double acc = 0.0, wgt = 0.0;
                 for (int i = 0; i < nc; ++i) {
@@ -886,7 +903,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
                 }
             }
             if (do_eval) {
-                const int nc = sm.nch[q];
+                const int nc = (sm.cb[q + 1] - sm.cb[q]);
                 const int cbq = sm.cb[q] - sm.cb[q0];
                 for (int i = 0; i < nc; ++i) {
                     const int cc = cbq + i;
@@ -1149,7 +1166,7 @@ template <int R, bool GEN>
 cudaError_t launch_tiles(const KParams& kp, cudaStream_t st) {
     using G = WT<R>;
     const uint32_t ph = GEN ? kp.phases : (PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE);
-    const WLayout L = make_wlayout<R>(ph, GEN ? kp.p.flags : (kp.p.flags & WOIT_NORMALIZE));
+    const WLayout L = make_wlayout<R>(ph, GEN ? kp.p.flags : (kp.p.flags & WOIT_NORMALIZE), !GEN && WOIT_ALIASZ);
     const int bytes = (int)(L.total * G::WPB);
     cudaError_t err = cudaFuncSetAttribute(frame_kernel<R, GEN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (err != cudaSuccess) return err;

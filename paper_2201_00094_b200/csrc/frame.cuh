@@ -34,6 +34,7 @@ struct KParams {
     int32_t use_tma;
     int64_t* long_list;  // [0] = count, [1..] = band-local pixel ids
     int64_t long_cap;
+    unsigned long long* win_counter;  // dynamic window claims (zeroed per launch)
 };
 
 // per-rank warp-tile geometry
@@ -50,15 +51,17 @@ struct WT {
 };
 
 struct WLayout {
-    uint32_t offs, nch, cb, rot, nearu, faru, lo, den, rcp, vtot, chunk;
+    uint32_t offs, cb, nearu, faru, lo, den, rcp, vtot, chunk;
     uint32_t depth, alpha, trans, rad, ior, normal, bf, zfix, part, cells, coef32, accp, pk, opq, bar, total;
 };
 
 WOIT_HD uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
 
-// shared-memory slice of one warp (bytes); the CTA holds WPB slices
+// shared-memory slice of one warp (bytes); the CTA holds WPB slices. alias_z: the
+// fixed-point z overwrites the staged depth in place (fast path: the build computes
+// z and nothing reads the depth afterwards), saving the separate [FBW] array.
 template <int R>
-WOIT_HD WLayout make_wlayout(uint32_t phases, int flags) {
+WOIT_HD WLayout make_wlayout(uint32_t phases, int flags, bool alias_z) {
     using G = WT<R>;
     const bool at = phases & (PH_BUILD | PH_EVAL);
     const bool ev = phases & PH_EVAL;
@@ -70,15 +73,17 @@ WOIT_HD WLayout make_wlayout(uint32_t phases, int flags) {
     WLayout L;
     uint32_t o = 0;
     L.offs = o;  o = align16(o + 8u * (G::WIN + 1));
-    L.nch = o;   o = align16(o + 4u * G::WIN);
-    L.cb = o;    o = align16(o + 4u * (G::WIN + 1));
-    L.rot = o;   o = align16(o + 4u * G::WIN);
-    L.nearu = o; o = align16(o + 4u * G::WIN);
-    L.faru = o;  o = align16(o + 4u * G::WIN);
-    L.lo = o;    o = align16(o + 8u * G::WIN);
-    L.den = o;   o = align16(o + 8u * G::WIN);
-    L.rcp = o;   o = align16(o + 8u * G::WIN);
-    L.vtot = o;  o = align16(o + 8u * 3 * G::WIN);
+    L.cb = o;    o = align16(o + 4u * (G::WIN + 1));  // chunk prefix (chunks of q = cb[q+1] - cb[q])
+    // per sub-tile pixel (<= SUBP)
+    L.nearu = o; o = align16(o + 4u * G::SUBP);
+    L.faru = o;  o = align16(o + 4u * G::SUBP);
+    // depth maps and exp(-A_total) [SUBP][3]; during the build these contiguous
+    // bytes (>= 384) are the [3][32] float sink of the dropped D_M terms
+    L.lo = o;    o = align16(o + 8u * G::SUBP);
+    L.den = o;   o = align16(o + 8u * G::SUBP);
+    L.rcp = o;   o = align16(o + 8u * G::SUBP);
+    L.vtot = o;  o = align16(o + 8u * 3 * G::SUBP);
+    static_assert(8 * 6 * G::SUBP >= 4 * 3 * 32, "sink overlay too small");
     L.chunk = o; o = align16(o + 4u * 32);
     L.depth = o; o = align16(o + 4u * FS);
     L.alpha = o; o = align16(o + (at ? 4u * FS : 0u));
@@ -87,7 +92,8 @@ WOIT_HD WLayout make_wlayout(uint32_t phases, int flags) {
     L.ior = o;   o = align16(o + (need_ior ? 4u * FS : 0u));
     L.normal = o; o = align16(o + (need_nrm ? 12u * FS : 0u));
     L.bf = o;    o = align16(o + (need_bf ? (uint32_t)G::FBW + 32u : 0u));
-    L.zfix = o;  o = align16(o + (at ? 4u * G::FBW : 0u));
+    L.zfix = alias_z ? L.depth : o;
+    o = align16(o + (at && !alias_z ? 4u * G::FBW : 0u));
     // one region, reused: chunk partials [M][3][32] (per-cell differences D) during the
     // build, then the sub-tile's coefficients [SUBP][V], cell staircase [SUBP][VR]
     // and chunk accumulators [9][32]
@@ -99,9 +105,12 @@ WOIT_HD WLayout make_wlayout(uint32_t phases, int flags) {
     L.cells = L.part + align16(4u * G::SUBP * G::V);
     L.accp = L.cells + align16(8u * G::SUBP * CR);
     L.pk = o;    o = align16(o + (packed ? 8u * G::WIN * G::V : 0u));
-    L.opq = o;   o = align16(o + 12u * (G::SUBP + 8));
+    L.opq = o;   o = align16(o + 12u * (G::SUBP + 4));  // [pa & ~3, pb rounded up to 4)
     L.bar = o;   o = align16(o + 16u);
-    L.total = (o + 127u) & ~127u;
+#ifdef WOIT_SMEM_PAD
+    o += WOIT_SMEM_PAD;
+#endif
+    L.total = align16(o);
     return L;
 }
 

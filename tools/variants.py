@@ -10,7 +10,7 @@ import subprocess
 import sys
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-VDIR = os.path.join(REPO, "build", "variants")
+VDIR = os.path.join(REPO, "variants_lib")  # git-ignored, travels with gpurun (build/ does not)
 
 
 def do_build(specs):

@@ -262,6 +262,7 @@ def run_ours(args, cfg):
         except Exception:
             args.traffic = None
     alg = algorithmic_bytes(P, n, cfg["rank"])
+    frame_in_bytes = n * 32 + (P + 1) * 8 + P * 12  # depth, alpha, T, L + offsets + opaque RGB
     achieved = alg / (kern_ms * 1e-3) / 1e9
     clocks = clk.summary()
     if rank != 0:
@@ -278,7 +279,7 @@ def run_ours(args, cfg):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32 (z, indices and per-pixel sums in f64)", "data": "synthetic",
         "config": {"workload": cfg["name"], "width": Wd, "height": frame_h, "frag_per_px": cfg["layers"],
-                   "rank": cfg["rank"], "fragments": frags_total, "l2_flush": "inputs 2.1 GB/GPU > 126 MB L2",
+                   "rank": cfg["rank"], "fragments": frags_total, "l2_flush": f"inputs {frame_in_bytes / 1e9:.1f} GB/GPU > 126 MB L2",
                    "parallelism": f"row bands x{world}, NCCL image all-gather" if world > 1 else "1 GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": args.traffic,

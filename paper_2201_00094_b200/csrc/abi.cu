@@ -38,6 +38,22 @@ int check_frags(const woit_frags_t* f, bool need_frag_arrays) {
     return WOIT_OK;
 }
 
+// aberration taps for the kernels (frame.cuh TapTable), with the reference's f64
+// operation order (spectral_weight's host branch keeps every rounding)
+void fill_taps(KParams& kp) {
+    const int k = kp.p.aberration_taps;
+    kp.taps.n = 0;
+    kp.taps.pad = 0;
+    if (!(kp.p.flags & WOIT_CHROMATIC_ABERRATION) || k < 3 || k > kMaxTapTable) return;
+    const bool lit = kp.p.flags & WOIT_LITERAL_SPECTRAL_T;
+    for (int i = 0; i < k; ++i) {
+        spectral_weight(i, k, lit, kp.taps.w[i]);
+        volatile double two_i = 2.0 * i;
+        kp.taps.fac[i] = two_i / (double)(k - 1);
+    }
+    kp.taps.n = k;
+}
+
 int run_frame(const woit_frags_t* f, const woit_params_t* p, woit_bufs_t* b, uint32_t phases, void* ws,
               size_t ws_bytes, void* stream) {
     if (!b) return WOIT_EINVAL;
@@ -56,6 +72,7 @@ int run_frame(const woit_frags_t* f, const woit_params_t* p, woit_bufs_t* b, uin
     kp.p = *p;
     kp.b = *b;
     kp.phases = phases;
+    fill_taps(kp);
     const void* ptrs[] = {f->depth, f->alpha, f->trans, f->radiance, f->normal, f->ior, f->backface, b->vhat,
                           f->opaque_color};
     bool al = true;
@@ -154,6 +171,7 @@ int woit_step4_composite(const woit_frags_t* frags, const woit_params_t* params,
     kp.p = *params;
     kp.b = *bufs;
     kp.phases = PH_COMPOSITE;
+    fill_taps(kp);
     kp.use_tma = 0;
     kp.long_list = nullptr;
     kp.long_cap = 0;

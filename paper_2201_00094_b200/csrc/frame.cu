@@ -885,64 +885,50 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
                     kp.b.refraction_offset[p * 2 + 1] = 0.0f;
                 }
             }
-        } else if (lane < nqs) {
-            const int q = q0 + lane;
+        } else if (lane < 3 * nqs) {
+            // general path: one lane per (pixel, channel) as well; the refraction and
+            // diffusion sums are per pixel, and every channel lane forms them in the
+            // same order (identical values); the channel-0 lane stores them
+            const int kch = lane / nqs, kq = lane - kch * nqs;
+            const int q = q0 + kq;
             const int64_t p = w0 + q;
-            double acc[3] = {0, 0, 0}, wgt[3] = {0, 0, 0}, ro[2] = {0, 0}, dsum = 0.0, dp = 0.0;
-            const bool acc_in = GEN && ((ph & PH_EVAL_ACC) || ((ph & PH_COMPOSITE) && !do_eval));
-            if (acc_in && diffuse && kp.b.diffusion) dp = kp.b.diffusion[p];
+            double acc = 0.0, wgt = 0.0, ro0 = 0.0, ro1 = 0.0, dsum = 0.0, dp = 0.0;
+            const bool acc_in = (ph & PH_EVAL_ACC) || ((ph & PH_COMPOSITE) && !do_eval);
             if (acc_in) {
-#pragma unroll
-                for (int ch = 0; ch < 3; ++ch) {
-                    acc[ch] = kp.b.accum[p * 3 + ch];
-                    wgt[ch] = kp.b.weight[p * 3 + ch];
-                }
+                acc = kp.b.accum[p * 3 + kch];
+                wgt = kp.b.weight[p * 3 + kch];
                 if (kp.b.refraction_offset) {
-                    ro[0] = kp.b.refraction_offset[p * 2];
-                    ro[1] = kp.b.refraction_offset[p * 2 + 1];
+                    ro0 = kp.b.refraction_offset[p * 2];
+                    ro1 = kp.b.refraction_offset[p * 2 + 1];
                 }
+                if (diffuse && kp.b.diffusion) dp = kp.b.diffusion[p];
             }
             if (do_eval) {
                 const int nc = (sm.cb[q + 1] - sm.cb[q]);
                 const int cbq = sm.cb[q] - sm.cb[q0];
                 for (int i = 0; i < nc; ++i) {
                     const int cc = cbq + i;
-#pragma unroll
-                    for (int ch = 0; ch < 3; ++ch) {
-                        acc[ch] += (double)sm.accp[ch * WC + cc];
-                        wgt[ch] += (double)sm.accp[(3 + ch) * WC + cc];
-                    }
+                    acc += (double)sm.accp[kch * WC + cc];
+                    wgt += (double)sm.accp[(3 + kch) * WC + cc];
                     if (refr) {
-                        ro[0] += (double)sm.accp[6 * WC + cc];
-                        ro[1] += (double)sm.accp[7 * WC + cc];
+                        ro0 += (double)sm.accp[6 * WC + cc];
+                        ro1 += (double)sm.accp[7 * WC + cc];
                     }
                     if (diffuse) dsum += (double)sm.accp[8 * WC + cc];
                 }
-                if (diffuse) {
-                    dp = dadd(dp, ddiv(dsum, 3.0));
-                    if (kp.b.diffusion) kp.b.diffusion[p] = (float)dp;
-                }
-                if (kp.b.accum)
-                    for (int ch = 0; ch < 3; ++ch) kp.b.accum[p * 3 + ch] = (float)acc[ch];
-                if (kp.b.weight)
-                    for (int ch = 0; ch < 3; ++ch) kp.b.weight[p * 3 + ch] = (float)wgt[ch];
-                if (kp.b.refraction_offset) {
-                    kp.b.refraction_offset[p * 2] = (float)ro[0];
-                    kp.b.refraction_offset[p * 2 + 1] = (float)ro[1];
+                if (diffuse) dp = dadd(dp, ddiv(dsum, 3.0));
+                if (kp.b.accum) kp.b.accum[p * 3 + kch] = (float)acc;
+                if (kp.b.weight) kp.b.weight[p * 3 + kch] = (float)wgt;
+                if (kch == 0) {
+                    if (diffuse && kp.b.diffusion) kp.b.diffusion[p] = (float)dp;
+                    if (kp.b.refraction_offset) {
+                        kp.b.refraction_offset[p * 2] = (float)ro0;
+                        kp.b.refraction_offset[p * 2 + 1] = (float)ro1;
+                    }
                 }
             }
-            if ((ph & PH_COMPOSITE) && kp.b.output) {
-                float out[3];
-                if (GEN) {
-                    composite_pixel(kp, p, acc, wgt, ro[0], ro[1], sm.vtot + 3 * lane, dp, out);
-                } else {
-                    const int si = (int)(p - ((w0 + q0) & ~(int64_t)3));
-                    const float bgc[3] = {sm.opq[3 * si], sm.opq[3 * si + 1], sm.opq[3 * si + 2]};
-                    composite_plain(flags, bgc, acc, wgt, sm.vtot + 3 * lane, out);
-                }
-#pragma unroll
-                for (int ch = 0; ch < 3; ++ch) kp.b.output[p * 3 + ch] = out[ch];
-            }
+            if ((ph & PH_COMPOSITE) && kp.b.output)
+                kp.b.output[p * 3 + kch] = composite_channel(kp, p, kch, acc, wgt, ro0, ro1, sm.vtot[kq * 3 + kch], dp);
         }
         fence_proxy_async();
         __syncwarp();

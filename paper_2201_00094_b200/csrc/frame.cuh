@@ -26,6 +26,17 @@ enum : uint32_t {
     PH_COMPOSITE = 64u,   // output
 };
 
+// Aberration taps tabulated on the host (pipeline.py:226-239, 258-281): the
+// spectral weights and positions depend only on (i, k, literal), so the kernels
+// read them instead of recomputing three f64 divisions per tap per pixel.
+constexpr int kMaxTapTable = 65;
+struct TapTable {
+    int32_t n;  // taps tabulated; 0 (k > kMaxTapTable): computed in the kernel
+    int32_t pad;
+    double fac[kMaxTapTable];   // 2 i / (k - 1)
+    double w[kMaxTapTable][3];  // spectral_weight(i, k)
+};
+
 struct KParams {
     woit_frags_t f;
     woit_params_t p;
@@ -35,6 +46,7 @@ struct KParams {
     int64_t* long_list;  // [0] = count, [1..] = band-local pixel ids
     int64_t long_cap;
     unsigned long long* win_counter;  // dynamic window claims (zeroed per launch)
+    TapTable taps;
 };
 
 // per-rank warp-tile geometry
@@ -117,20 +129,43 @@ WOIT_HD WLayout make_wlayout(uint32_t phases, int flags, bool alias_z) {
 // ---------------------------------------------------------------------------
 // composite of one pixel (pipeline.py:242-308)
 
-WOIT_D double smoothstep_d(double e0, double e1, double x) {
-    double u = (x - e0) / (e1 - e0);
+// smoothstep / spectral_weight (pipeline.py:220-239) with explicit round-to-nearest
+// operations (no FMA contraction), i.e. exactly the reference's f64 arithmetic. The
+// host tabulates the same formulas (abi.cu fill_taps); this is the k > 65 fallback.
+WOIT_HD double smoothstep_d(double e0, double e1, double x) {
+#ifdef __CUDA_ARCH__
+    double u = ddiv(dsub(x, e0), dsub(e1, e0));
     u = fmin(1.0, fmax(0.0, u));
-    return u * u * (3.0 - 2.0 * u);
+    return dmul(dmul(u, u), dsub(3.0, dmul(2.0, u)));
+#else
+    volatile double d = e1 - e0;  // volatile: keep every rounding step
+    double u = (x - e0) / d;
+    u = u < 0.0 ? 0.0 : u;
+    u = u > 1.0 ? 1.0 : u;
+    volatile double uu = u * u;
+    volatile double r = 3.0 - 2.0 * u;
+    return uu * r;
+#endif
 }
 
-// spectral_weight (pipeline.py:226-239)
-WOIT_D void spectral_weight(int i, int k, bool literal, double w[3]) {
-    const double t = literal ? 0.5 + 2.0 * i / (double)(k - 1) : i / (double)(k - 1);
+WOIT_HD void spectral_weight(int i, int k, bool literal, double w[3]) {
+#ifdef __CUDA_ARCH__
+    const double q = ddiv(dmul(2.0, (double)i), (double)(k - 1));
+    const double t = literal ? dadd(0.5, q) : ddiv((double)i, (double)(k - 1));
     const double wr = smoothstep_d(0.5, 1.0 / 3.0, t);
     const double wb = smoothstep_d(0.5, 2.0 / 3.0, t);
     w[0] = wr;
-    w[1] = 1.0 - wr - wb;
+    w[1] = dsub(dsub(1.0, wr), wb);
     w[2] = wb;
+#else
+    const double t = literal ? 0.5 + 2.0 * i / (double)(k - 1) : i / (double)(k - 1);
+    const double wr = smoothstep_d(0.5, 1.0 / 3.0, t);
+    const double wb = smoothstep_d(0.5, 2.0 / 3.0, t);
+    volatile double g = 1.0 - wr;
+    w[0] = wr;
+    w[1] = g - wb;
+    w[2] = wb;
+#endif
 }
 
 // bilinear_sample (pipeline.py:242-255): edge clamped, in f64
@@ -154,20 +189,69 @@ WOIT_D void bilinear(const float* __restrict__ img, int W, int H, double x, doub
     }
 }
 
+// one channel of bilinear(): the same operations for that channel
+WOIT_D double bilinear_ch(const float* __restrict__ img, int W, int H, double x, double y, int ch) {
+    x = fmin(fmax(x, 0.0), (double)W - 1.0);
+    y = fmin(fmax(y, 0.0), (double)H - 1.0);
+    const double fx = floor(x), fy = floor(y);
+    const int x0 = (int)fx, y0 = (int)fy;
+    const int x1 = min(x0 + 1, W - 1), y1 = min(y0 + 1, H - 1);
+    const double tx = x - fx, ty = y - fy;
+    const double a = img[((int64_t)y0 * W + x0) * 3 + ch], b = img[((int64_t)y0 * W + x1) * 3 + ch];
+    const double c = img[((int64_t)y1 * W + x0) * 3 + ch], d = img[((int64_t)y1 * W + x1) * 3 + ch];
+    const double top = dadd(dmul(a, 1.0 - tx), dmul(b, tx));
+    const double bot = dadd(dmul(c, 1.0 - tx), dmul(d, tx));
+    return dadd(dmul(top, 1.0 - ty), dmul(bot, ty));
+}
+
+WOIT_D void tap(const TapTable& tt, int i, int k, bool lit, double& fac, double w[3]) {
+    if (tt.n == k) {
+        fac = tt.fac[i];
+        w[0] = tt.w[i][0];
+        w[1] = tt.w[i][1];
+        w[2] = tt.w[i][2];
+    } else {
+        spectral_weight(i, k, lit, w);
+        fac = ddiv(dmul(2.0, (double)i), (double)(k - 1));
+    }
+}
+
+// Channel `ch` of the background of one pixel (pipeline.py:290-303); see sample_background.
+WOIT_D double sample_background_ch(const float* img, int W, int H, int64_t gp, int flags, int taps,
+                                   const TapTable& tt, double ox, double oy, int ch) {
+    if (flags & (WOIT_CHROMATIC_ABERRATION | WOIT_REFRACTION)) {
+        const double px = (double)(gp % W), py = (double)(gp / W);
+        if (flags & WOIT_CHROMATIC_ABERRATION) {
+            const bool lit = flags & WOIT_LITERAL_SPECTRAL_T;
+            double num = 0.0, den = 0.0;
+            for (int i = 0; i < taps; ++i) {
+                double w[3], fac;
+                tap(tt, i, taps, lit, fac, w);
+                if (w[ch] != 0.0)  // w s adds exactly 0 otherwise (s is finite)
+                    num = dadd(num, dmul(w[ch], bilinear_ch(img, W, H, dadd(px, dmul(ox, fac)),
+                                                            dadd(py, dmul(oy, fac)), ch)));
+                den = dadd(den, w[ch]);
+            }
+            return den > 0.0 ? ddiv(num, den) : bilinear_ch(img, W, H, dadd(px, ox), dadd(py, oy), ch);
+        }
+        return bilinear_ch(img, W, H, dadd(px, ox), dadd(py, oy), ch);
+    }
+    return (double)img[gp * 3 + ch];
+}
+
 // Background of one pixel read from `img` (pipeline.py:290-303): the k-tap aberration
 // gather, a bilinear sample at the refracted position, or the pixel itself. `img` is
 // [H][W][3] addressed by the pixel id gp (global with a full image, else band-local).
 WOIT_D void sample_background(const float* img, int W, int H, int64_t gp, int flags, int taps,
-                              double ox, double oy, double bg[3]) {
+                              const TapTable& tt, double ox, double oy, double bg[3]) {
     if (flags & (WOIT_CHROMATIC_ABERRATION | WOIT_REFRACTION)) {
         const double px = (double)(gp % W), py = (double)(gp / W);
         if (flags & WOIT_CHROMATIC_ABERRATION) {
             const bool lit = flags & WOIT_LITERAL_SPECTRAL_T;
             double num[3] = {0.0, 0.0, 0.0}, den[3] = {0.0, 0.0, 0.0};
             for (int i = 0; i < taps; ++i) {
-                double w[3], s[3];
-                spectral_weight(i, taps, lit, w);
-                const double fac = 2.0 * i / (double)(taps - 1);
+                double w[3], s[3], fac;
+                tap(tt, i, taps, lit, fac, w);
                 bilinear(img, W, H, dadd(px, dmul(ox, fac)), dadd(py, dmul(oy, fac)), s);
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) {
@@ -209,7 +293,7 @@ WOIT_D void composite_pixel(const KParams& kp, int64_t p, const double acc[3],
     const int64_t gp = full ? kp.f.pixel_base + p : p;
     if (gather) {
         sample_background(full ? kp.b.full_opaque_image : kp.f.opaque_color, W, H, gp, flags,
-                          kp.p.aberration_taps, ox, oy, bg);
+                          kp.p.aberration_taps, kp.taps, ox, oy, bg);
     } else {
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) bg[ch] = (double)kp.f.opaque_color[p * 3 + ch];
@@ -217,7 +301,7 @@ WOIT_D void composite_pixel(const KParams& kp, int64_t p, const double acc[3],
     if (flags & WOIT_DIFFUSION) {
         // K_resolve: lerp towards the same sample of the blurred background
         double bb[3];
-        sample_background(kp.b.blurred_image, W, H, gp, flags, kp.p.aberration_taps, ox, oy, bb);
+        sample_background(kp.b.blurred_image, W, H, gp, flags, kp.p.aberration_taps, kp.taps, ox, oy, bb);
         const double w = diffusion_weight(kp, dp);
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) bg[ch] = dadd(bg[ch], dmul(w, dsub(bb[ch], bg[ch])));
@@ -247,6 +331,31 @@ WOIT_D void composite_plain(int flags, const float bgc[3], const double acc[3], 
             out[ch] = (float)dadd(acc[ch], dmul(bg, vtot[ch]));
         }
     }
+}
+
+// Channel `ch` of composite_pixel, for per-(pixel, channel) lanes: the same
+// operations, so the result is bit-identical to composite_pixel's channel.
+WOIT_D float composite_channel(const KParams& kp, int64_t p, int ch, double acc, double wgt, double ox,
+                               double oy, double vt, double dp) {
+    const int W = kp.f.width;
+    const int flags = kp.p.flags;
+    const bool gather = flags & (WOIT_CHROMATIC_ABERRATION | WOIT_REFRACTION);
+    const bool full = kp.b.full_opaque_image != nullptr;
+    const int H = full ? kp.f.height : (int)(kp.f.npix / W);
+    const int64_t gp = full ? kp.f.pixel_base + p : p;
+    double bg = gather ? sample_background_ch(full ? kp.b.full_opaque_image : kp.f.opaque_color, W, H, gp,
+                                              flags, kp.p.aberration_taps, kp.taps, ox, oy, ch)
+                       : (double)kp.f.opaque_color[p * 3 + ch];
+    if (flags & WOIT_DIFFUSION) {
+        const double bb = sample_background_ch(kp.b.blurred_image, W, H, gp, flags, kp.p.aberration_taps,
+                                               kp.taps, ox, oy, ch);
+        bg = dadd(bg, dmul(diffusion_weight(kp, dp), dsub(bb, bg)));
+    }
+    if (flags & WOIT_NORMALIZE) {
+        const double avg = ddiv(acc, fmax(kNormEps, wgt));
+        return (float)dadd(dmul(avg, 1.0 - vt), dmul(bg, vt));
+    }
+    return (float)dadd(acc, dmul(bg, vt));
 }
 
 // Primary ray direction of global pixel gp (scene.py:199-212), f64.

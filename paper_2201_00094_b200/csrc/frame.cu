@@ -251,6 +251,43 @@ WOIT_D void eval_chunk_fast(const zfix_t* __restrict__ zf, const float* __restri
 // storage (the headline configuration); GEN=true covers every flag and the
 // step-wise entry points.
 
+// A run of `ne` fragment-free pixels starting at band pixel p0, in the fused frame:
+// lane l finishes pixel p0 + l with the values the full phases would produce for
+// an empty pixel -- bounds (+inf, -inf), zero coefficients (packed: slot 0 +0,
+// the others -0, as the E5B9G9R9 round trip of 0), zero accumulators and offset,
+// and the composite with acc = wgt = 0, v_tot = 1, offset 0, D = 0, i.e. the
+// background itself -- without staging, chunks or the per-(pixel, channel) phases.
+template <int R, bool GEN>
+WOIT_D void empty_run(const KParams& kp, int64_t p0, int ne, int lane) {
+    constexpr int V = 3 * (2 << R);
+    const int flags = GEN ? kp.p.flags : (kp.p.flags & WOIT_NORMALIZE);
+    if (kp.b.coeffs) {
+        float* c = kp.b.coeffs + p0 * V;
+        const bool packed = GEN && (flags & WOIT_PACKED_STORAGE);
+        for (int i = lane; i < ne * V; i += 32) c[i] = (packed && (i % V) >= 3) ? -0.0f : 0.0f;
+    }
+    if (lane >= ne) return;
+    const int64_t p = p0 + lane;
+    if (kp.b.near) kp.b.near[p] = INFINITY;
+    if (kp.b.far) kp.b.far[p] = -INFINITY;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        if (kp.b.accum) kp.b.accum[p * 3 + ch] = 0.0f;
+        if (kp.b.weight) kp.b.weight[p * 3 + ch] = 0.0f;
+    }
+    if (kp.b.refraction_offset) {
+        kp.b.refraction_offset[p * 2] = 0.0f;
+        kp.b.refraction_offset[p * 2 + 1] = 0.0f;
+    }
+    if (GEN && (flags & WOIT_DIFFUSION) && kp.b.diffusion) kp.b.diffusion[p] = 0.0f;
+    if (kp.b.output) {
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch)
+            kp.b.output[p * 3 + ch] = GEN ? composite_channel(kp, p, ch, 0.0, 0.0, 0.0, 0.0, 1.0, 0.0)
+                                          : kp.f.opaque_color[p * 3 + ch];
+    }
+}
+
 template <int R, bool GEN>
 struct WSmem {
     int64_t* offs;     // [WIN+1] window CSR offsets
@@ -379,6 +416,8 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
     __syncwarp();
     // chunks per pixel, window prefix (warp scan) and combine rotation
     int my_nch = 0;
+    // any fragment-free pixel in this window? (enables the empty-run shortcut below)
+    const bool any_empty = __any_sync(0xffffffffu, lane < nq && sm.offs[lane + 1] == sm.offs[lane]);
     if (lane < nq) {
         const int64_t run = sm.offs[lane + 1] - sm.offs[lane];
         const int64_t nc64 = (run + CH - 1) / CH;
@@ -396,6 +435,17 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
 
     int q0 = 0;
     while (q0 < nq) {
+        if (ph == kFused && any_empty) {
+            // leading fragment-free pixels: finished directly, 32 per pass
+            const bool emp = q0 + lane < nq && sm.offs[q0 + lane + 1] == sm.offs[q0 + lane];
+            const unsigned em = __ballot_sync(0xffffffffu, emp);
+            const int ne = em == 0xffffffffu ? 32 : __ffs(~em) - 1;
+            if (ne > 0) {
+                empty_run<R, GEN>(kp, w0 + q0, ne, lane);
+                q0 += ne;
+                continue;
+            }
+        }
         // sub-tile end: largest q1 with <= FBW fragments and <= 32 chunks
         const int cand = lane + 1;
         const bool fits = cand > q0 && cand <= nq && cand - q0 <= SUBP &&

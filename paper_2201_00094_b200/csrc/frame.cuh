@@ -221,6 +221,21 @@ WOIT_D double sample_background_ch(const float* img, int W, int H, int64_t gp, i
                                    const TapTable& tt, double ox, double oy, int ch) {
     if (flags & (WOIT_CHROMATIC_ABERRATION | WOIT_REFRACTION)) {
         const double px = (double)(gp % W), py = (double)(gp / W);
+        if (ox == 0.0 && oy == 0.0) {
+            // every tap lands on the pixel itself, where the bilinear weights are exactly
+            // (1, 0) and the sample is exactly the pixel: same arithmetic, no gathers
+            const double s0 = (double)img[gp * 3 + ch];
+            if (!(flags & WOIT_CHROMATIC_ABERRATION)) return s0;
+            const bool lit = flags & WOIT_LITERAL_SPECTRAL_T;
+            double num = 0.0, den = 0.0;
+            for (int i = 0; i < taps; ++i) {
+                double w[3], fac;
+                tap(tt, i, taps, lit, fac, w);
+                num = dadd(num, dmul(w[ch], s0));
+                den = dadd(den, w[ch]);
+            }
+            return den > 0.0 ? ddiv(num, den) : s0;
+        }
         if (flags & WOIT_CHROMATIC_ABERRATION) {
             const bool lit = flags & WOIT_LITERAL_SPECTRAL_T;
             double num = 0.0, den = 0.0;

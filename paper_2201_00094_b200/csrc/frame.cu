@@ -346,7 +346,10 @@ WOIT_D WSmem<R, GEN> wcarve(unsigned char* base, const WLayout& L) {
     return s;
 }
 
-template <int R, bool GEN>
+// FUS: the phases are the fused render's (compile-time constant), so the
+// step-wise accumulate / from-buffer branches compile out; GEN && !FUS serves the
+// step1..step4 entry points.
+template <int R, bool GEN, bool FUS>
 __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel(const KParams kp) {
     using G = WT<R>;
     constexpr int S = G::S, V = G::V, CH = G::CH, WC = 32, FBW = G::FBW, WIN = G::WIN, SUBP = G::SUBP;
@@ -354,7 +357,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
     constexpr int M = S;       // cells
     constexpr uint32_t kFused = PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const uint32_t ph = GEN ? kp.phases : kFused;
+    const uint32_t ph = (GEN && !FUS) ? kp.phases : kFused;
     const int flags = GEN ? kp.p.flags : (kp.p.flags & WOIT_NORMALIZE);
     const WLayout L = make_wlayout<R>(ph, flags, !GEN && WOIT_ALIASZ);
     const int lane = threadIdx.x & 31;
@@ -1198,13 +1201,13 @@ size_t long_smem_bytes() {
     return (size_t)V * TL * 8 + (size_t)V * 8 + (size_t)V * 4;
 }
 
-template <int R, bool GEN>
+template <int R, bool GEN, bool FUS>
 cudaError_t launch_tiles(const KParams& kp, cudaStream_t st) {
     using G = WT<R>;
-    const uint32_t ph = GEN ? kp.phases : (PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE);
+    const uint32_t ph = (GEN && !FUS) ? kp.phases : (PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE);
     const WLayout L = make_wlayout<R>(ph, GEN ? kp.p.flags : (kp.p.flags & WOIT_NORMALIZE), !GEN && WOIT_ALIASZ);
     const int bytes = (int)(L.total * G::WPB);
-    cudaError_t err = cudaFuncSetAttribute(frame_kernel<R, GEN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaError_t err = cudaFuncSetAttribute(frame_kernel<R, GEN, FUS>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (err != cudaSuccess) return err;
     // persistent grid: as many CTAs as can be resident, each warp loops over windows
     const int64_t warps = (kp.f.npix + G::WIN - 1) / G::WIN;
@@ -1212,14 +1215,14 @@ cudaError_t launch_tiles(const KParams& kp, cudaStream_t st) {
     int dev = 0, sms = 148, per_sm = 1;
     if (cudaGetDevice(&dev) == cudaSuccess)
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frame_kernel<R, GEN>, G::WPB * 32, bytes) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frame_kernel<R, GEN, FUS>, G::WPB * 32, bytes) !=
             cudaSuccess || per_sm < 1)
         per_sm = 1;
     cudaGetLastError();
     const int64_t resident = (int64_t)sms * per_sm * WOIT_PERSIST;
     if (WOIT_PERSIST > 0) grid = grid < resident ? grid : resident;
     if (grid > 0) {
-        frame_kernel<R, GEN><<<(unsigned)grid, G::WPB * 32, bytes, st>>>(kp);
+        frame_kernel<R, GEN, FUS><<<(unsigned)grid, G::WPB * 32, bytes, st>>>(kp);
         err = cudaGetLastError();
     }
     return err;
@@ -1229,8 +1232,10 @@ template <int R>
 cudaError_t launch_rank(const KParams& kp, cudaStream_t st) {
     using G = WT<R>;
     constexpr uint32_t kFused = PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE;
-    const bool fast = kp.phases == kFused && (kp.p.flags & ~WOIT_NORMALIZE) == 0;
-    cudaError_t err = fast ? launch_tiles<R, false>(kp, st) : launch_tiles<R, true>(kp, st);
+    const bool fused = kp.phases == kFused;
+    const bool fast = fused && (kp.p.flags & ~WOIT_NORMALIZE) == 0;
+    cudaError_t err = fast ? launch_tiles<R, false, true>(kp, st)
+                           : fused ? launch_tiles<R, true, true>(kp, st) : launch_tiles<R, true, false>(kp, st);
     if (err != cudaSuccess) return err;
     const size_t ls = long_smem_bytes<R>();
     err = cudaFuncSetAttribute(long_pixel_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ls);

@@ -172,6 +172,22 @@ int woit_build_atomic(const woit_frags_t* frags, const int32_t* pix, const woit_
 int woit_fragment_indices(const woit_frags_t* frags, const float* near, const float* far, int rank,
                           double* z, int32_t* slots, int32_t* cells, void* stream);
 
+/* ---- comparison methods (RenderConfig.method, baselines.py:135-220) ---------
+ * The reference's non-wavelet methods over the same CSR stream, in float64 with the
+ * reference's operation order (one thread per pixel), output fp32 [npix][3] over the
+ * opaque colour. WOIT_METHOD_ABUFFER is the exact sorted oracle (stable per-pixel sort
+ * by depth, then front to back); WBOIT uses wboit_weight = (gain, clamp lo, clamp hi);
+ * MLAB4 is the 4-node streaming blend. flags: WOIT_CUBE_TRANSMISSION only.
+ * wboit_weight is a HOST pointer to 3 doubles (read during the call).
+ * ABUFFER needs nfrag < 2^31 (segmented sort). */
+#define WOIT_METHOD_ABUFFER 1
+#define WOIT_METHOD_WBOIT 2
+#define WOIT_METHOD_MLAB4 3
+
+size_t woit_baseline_workspace_bytes(int method, int64_t npix, int64_t nfrag);
+int woit_render_baseline(const woit_frags_t* frags, int method, int flags, const double* wboit_weight,
+                         float* output, void* ws, size_t ws_bytes, void* stream);
+
 /* ---- K_resolve: the diffusion blur (in-repo definition, see WOIT_DIFFUSION) ----- */
 
 size_t woit_blur_workspace_bytes(int32_t width, int32_t height);

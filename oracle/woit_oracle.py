@@ -501,6 +501,78 @@ def step4_composite(bufs: OBuffers, cfg: OConfig, pixel_base: int = 0, full_img=
         bufs.output[:] = bufs.accum + bg * v_total
 
 
+# ---------------------------------------------------------------------------
+# comparison methods (RenderConfig.method != "wavelet"; baselines.py:135-220),
+# per-pixel Python loops: test-size inputs only
+
+WBOIT_WEIGHT = (10.0, 0.01, 3000.0)  # baselines.py:21
+WEIGHT_EPS = 1e-5                    # baselines.py:22
+
+
+def abuffer_frame(frame: OFrame, background, cube: bool = False) -> np.ndarray:
+    """Exact compositing in (depth, arrival) order, front to back (baselines.py:135-148)."""
+    t = frame.net_transmittance(cube)
+    c = frame.radiance * frame.alpha[:, None]
+    out = np.empty((frame.npix, 3))
+    for p in range(frame.npix):
+        s, e = int(frame.offsets[p]), int(frame.offsets[p + 1])
+        acc, vis = np.zeros(3), np.ones(3)
+        for i in s + np.argsort(frame.depth[s:e], kind="stable"):
+            acc = acc + c[i] * vis
+            vis = vis * t[i]
+        out[p] = acc + background[p] * vis
+    return out
+
+
+def wboit_frame(frame: OFrame, background, cube: bool = False, weight=WBOIT_WEIGHT) -> np.ndarray:
+    """Weighted blended OIT over the pixel's depth bounds (baselines.py:151-167)."""
+    gain, lo, hi = weight
+    t = frame.net_transmittance(cube)
+    out = np.empty((frame.npix, 3))
+    for p in range(frame.npix):
+        s, e = int(frame.offsets[p]), int(frame.offsets[p + 1])
+        d = frame.depth[s:e]
+        near, far = (d.min(), d.max()) if e > s else (np.inf, -np.inf)
+        rng = far - near
+        acc, wsum, rev = np.zeros(3), 0.0, np.ones(3)
+        for i in range(s, e):
+            z = (frame.depth[i] - near) / rng if rng > 0.0 else 0.5
+            z = min(max(z, 0.0), 1.0)
+            w = min(max(gain / (WEIGHT_EPS + z * z + np.power(z, 6)), lo), hi)
+            acc = acc + (w * frame.alpha[i]) * frame.radiance[i]
+            wsum = wsum + w * frame.alpha[i]
+            rev = rev * t[i]
+        avg = acc / max(1e-6, wsum)
+        out[p] = avg * (1.0 - rev) + background[p] * rev
+    return out
+
+
+def mlab_frame(frame: OFrame, background, k: int = 4, cube: bool = False) -> np.ndarray:
+    """k-node multi-layer alpha blending in arrival order (baselines.py:74-96, 170-220):
+    a node goes after every node at depth <= its own; k + 1 nodes merge the last two
+    (c = c1 + t1 c2, t = t1 t2); then front to back."""
+    if k < 2:
+        raise ValueError("mlab needs at least 2 slots")
+    t = frame.net_transmittance(cube)
+    c = frame.radiance * frame.alpha[:, None]
+    out = np.empty((frame.npix, 3))
+    for p in range(frame.npix):
+        nodes = []  # (depth, colour, transmittance)
+        for i in range(int(frame.offsets[p]), int(frame.offsets[p + 1])):
+            pos = sum(1 for n in nodes if n[0] <= frame.depth[i])
+            nodes.insert(pos, (frame.depth[i], c[i], t[i]))
+            if len(nodes) > k:
+                d1, c1, t1 = nodes[k - 1]
+                _, c2, t2 = nodes[k]
+                nodes[k - 1:] = [(d1, c1 + t1 * c2, t1 * t2)]
+        acc, vis = np.zeros(3), np.ones(3)
+        for _, cn, tn in nodes:
+            acc = acc + cn * vis
+            vis = vis * tn
+        out[p] = acc + background[p] * vis
+    return out
+
+
 def render_band(frame: OFrame, cfg: OConfig, cam: OCamera, full_img, p0: int, p1: int,
                 dirs=None, blurred_img=None) -> OBuffers:
     """One row band through the four passes (pipeline.py:321-330)."""

@@ -15,7 +15,7 @@ from .frame import FrameFragments  # noqa: F401
 from .pipeline import (METHODS, Camera, FrameBuffers, RayGrid, RenderConfig, Workspace,  # noqa: F401
                        camera_rays, eval_bounds, render_band, render_frame, step1_depth_bounds,
                        resolve_blur, step2_build, step2_build_atomic, step3_accumulate, step4_composite,
-                       pixel_ids)
+                       pixel_ids, render_baseline)
 from .packing import pack_rgb9e5, unpack_rgb9e5, roundtrip_coeff_array, bytes_per_pixel  # noqa: F401
 
 __version__ = "0.1.0"

@@ -31,6 +31,7 @@ PACKED_STORAGE = 0x10
 LITERAL_SPECTRAL_T = 0x20
 CUBE_BACKFACE_ONLY = 0x40
 DIFFUSION = 0x80
+METHOD_ABUFFER, METHOD_WBOIT, METHOD_MLAB4 = 1, 2, 3
 
 BUILD_BINNED = 0
 BUILD_ATOMIC = 1
@@ -76,6 +77,8 @@ _SIGS = {
     "woit_fragment_indices": (C.c_int, [C.POINTER(Frags), _vp, _vp, C.c_int, _vp, _vp, _vp, _vp]),
     "woit_blur_workspace_bytes": (_sz, [_i32, _i32]),
     "woit_build_atomic_workspace_bytes": (_sz, [_i64]),
+    "woit_baseline_workspace_bytes": (_sz, [C.c_int, _i64, _i64]),
+    "woit_render_baseline": (C.c_int, [C.POINTER(Frags), C.c_int, C.c_int, _vp, _vp, _vp, _sz, _vp]),
     "woit_build_atomic": (C.c_int, [C.POINTER(Frags), _vp, C.POINTER(Params), C.POINTER(Bufs), _vp, _sz, _vp]),
     "woit_resolve_blur": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _vp, _sz, _vp]),
     "woit_build_into_workspace_bytes": (_sz, [_i64, _i64]),

@@ -192,6 +192,25 @@ int woit_fragment_indices(const woit_frags_t* frags, const float* near, const fl
     return cuda_status(launch_indices(kp, z, slots, cells, static_cast<cudaStream_t>(stream)));
 }
 
+size_t woit_baseline_workspace_bytes(int method, int64_t npix, int64_t nfrag) {
+    if (method < WOIT_METHOD_ABUFFER || method > WOIT_METHOD_MLAB4 || npix < 0 || nfrag < 0) return 0;
+    return baseline_workspace(method, npix, nfrag);
+}
+
+int woit_render_baseline(const woit_frags_t* frags, int method, int flags, const double* wboit_weight, float* output,
+                         void* ws, size_t ws_bytes, void* stream) {
+    if (method < WOIT_METHOD_ABUFFER || method > WOIT_METHOD_MLAB4) return WOIT_EINVAL;
+    int s = check_frags(frags, true);
+    if (s) return s;
+    if (!output || !frags->opaque_color || (method == WOIT_METHOD_WBOIT && !wboit_weight)) return WOIT_EINVAL;
+    if (method == WOIT_METHOD_ABUFFER && frags->nfrag >= ((int64_t)1 << 31)) return WOIT_EINVAL;
+    if (!ws || ws_bytes < baseline_workspace(method, frags->npix, frags->nfrag)) return WOIT_EWORKSPACE;
+    const double zero[3] = {0.0, 0.0, 0.0};
+    return cuda_status(render_baseline(*frags, method, (flags & WOIT_CUBE_TRANSMISSION) != 0,
+                                       wboit_weight ? wboit_weight : zero, output, ws,
+                                       static_cast<cudaStream_t>(stream)));
+}
+
 size_t woit_build_atomic_workspace_bytes(int64_t npix) { return npix < 0 ? 0 : build_atomic_workspace(npix); }
 
 int woit_build_atomic(const woit_frags_t* frags, const int32_t* pix, const woit_params_t* params, woit_bufs_t* bufs,

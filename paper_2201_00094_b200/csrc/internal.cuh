@@ -23,6 +23,9 @@ cudaError_t pack(const double* v, int64_t n, uint32_t* words, cudaStream_t st);
 cudaError_t unpack(const uint32_t* words, int64_t n, double* out, cudaStream_t st);
 size_t blur_workspace(int32_t width, int32_t height);
 size_t build_atomic_workspace(int64_t npix);
+size_t baseline_workspace(int method, int64_t npix, int64_t nfrag);
+cudaError_t render_baseline(const woit_frags_t& f, int method, bool cube, const double wboit[3], float* out,
+                            void* ws, cudaStream_t st);
 cudaError_t build_atomic(const int32_t* pix, const woit_frags_t& f, int rank, int flags, const float* near,
                          const float* far, float* coeffs, void* ws, cudaStream_t st);
 cudaError_t resolve_blur(const float* image, int32_t W, int32_t H, int32_t r, float* out, void* ws,

@@ -13,8 +13,9 @@ Differences from the reference, all deliberate:
   are still computed in f64 / fixed point and are bit-identical;
 * ``render_frame`` needs ``frame=``: the analytic caster (scene.py:463-630) is
   out of scope, so there is no scene -> fragments step here;
-* only ``method="wavelet"`` renders; the A-buffer / WBOIT / MLAB baselines are
-  out of scope (SURVEY.md §2 row 9) and raise NotImplementedError;
+* the comparison methods (``method="abuffer" | "wboit" | "mlab4"``,
+  baselines.py:135-220) run as float64 per-pixel kernels (``render_baseline``);
+  they need ``frame=`` like the wavelet path;
 * ``diffusion`` / ``diffusion_radius`` (default off) add the north star's
   "resolve and blur" pass, which the reference does not have (SURVEY.md §8 row
   GAP): an in-repo definition, documented in include/woit.h (WOIT_DIFFUSION) and
@@ -23,6 +24,7 @@ Differences from the reference, all deliberate:
 
 from __future__ import annotations
 
+import ctypes as C
 import math
 from dataclasses import dataclass
 from typing import Optional, Tuple
@@ -34,7 +36,7 @@ from .frame import FrameFragments, ptr
 from .wavelet import TouchCounter
 
 METHODS = ("wavelet", "abuffer", "wboit", "mlab4")
-DEFAULT_WBOIT_WEIGHT = (1.0, 1.0, 1.0)
+DEFAULT_WBOIT_WEIGHT = (10.0, 0.01, 3000.0)  # baselines.py:21 (gain, clamp lo, clamp hi)
 _WORLD_UP = (0.0, 1.0, 0.0)   # scene.py:43
 _ALT_UP = (1.0, 0.0, 0.0)     # scene.py:44
 
@@ -409,13 +411,12 @@ def render_frame(scene, cfg: RenderConfig, counter: Optional[TouchCounter] = Non
     Camera, or None for the default). ``workers > 1`` renders that many row bands
     one after another; the result is bit-identical to one band.
     """
-    if cfg.method != "wavelet":
-        raise NotImplementedError(f"method {cfg.method!r} is out of scope for the B200 path "
-                                  "(only the wavelet compositor is built)")
     if frame is None:
         raise NotImplementedError("scene casting (scene.py:463-630) is out of scope: pass frame=")
     if frame.npix != cfg.width * cfg.height:
         raise ValueError("frame size does not match the config")
+    if cfg.method != "wavelet":
+        return render_baseline(frame, cfg).reshape(cfg.height, cfg.width, 3)
     cam = getattr(scene, "camera", scene) if scene is not None else None
     rays = camera_rays(cam if isinstance(cam, Camera) else _as_camera(cam), cfg.width, cfg.height)
     full_img = frame.opaque_color.reshape(cfg.height, cfg.width, 3)
@@ -433,6 +434,27 @@ def render_frame(scene, cfg: RenderConfig, counter: Optional[TouchCounter] = Non
         bufs = render_band(band, cfg, rays, full_opaque_image=full_img, counter=counter, blurred_image=blurred)
         out[p0:p1] = bufs.output
     return out.reshape(cfg.height, cfg.width, 3)
+
+
+_METHOD_IDS = {"abuffer": _lib.METHOD_ABUFFER, "wboit": _lib.METHOD_WBOIT, "mlab4": _lib.METHOD_MLAB4}
+
+
+def render_baseline(frame: FrameFragments, cfg: RenderConfig, ws: Optional[Workspace] = None) -> torch.Tensor:
+    """The reference's comparison methods over a frame (pipeline.py:341-354 ->
+    baselines.abuffer_frame / wboit_frame / mlab_frame): (npix, 3) fp32 over the
+    opaque colour, computed per pixel in float64."""
+    if cfg.method not in _METHOD_IDS:
+        raise ValueError(f"{cfg.method!r} is not a comparison method")
+    lib = _lib.load()
+    method = _METHOD_IDS[cfg.method]
+    out = torch.empty(frame.npix, 3, dtype=torch.float32, device=frame.device)
+    n = lib.woit_baseline_workspace_bytes(method, frame.npix, frame.nfrag)
+    t = (ws or _WS).get(n, frame.device)
+    wb = (C.c_double * 3)(*[float(x) for x in cfg.wboit_weight])
+    flags = _lib.CUBE_TRANSMISSION if cfg.cube_transmission else 0
+    _lib.check(lib.woit_render_baseline(frame.c_struct(), method, flags, C.cast(wb, C.c_void_p), ptr(out),
+                                        ptr(t), t.numel(), _stream()), "render_baseline")
+    return out
 
 
 def _as_camera(cam) -> Camera:

@@ -143,7 +143,50 @@ def kernel_case():
          triples=triples, words=words, packed_rt=packed_rt)
 
 
+def baselines_case():
+    """The reference's comparison methods (baselines.py:135-220) on fp32-exact inputs:
+    synthetic streams, and scene streams rounded to fp32 (so sort order and ties are
+    the device's). Reference near/far for WBOIT as pipeline.render_frame computes them."""
+    from woit import baselines as rb
+
+    def f32_frame(fr):
+        r = lambda a: np.asarray(np.asarray(a, dtype=np.float32), dtype=np.float64)
+        return FrameFragments(fr.width, fr.height, fr.pixel, r(fr.depth), r(fr.alpha), r(fr.trans), r(fr.radiance),
+                              r(fr.normal), r(fr.ior), fr.backface, fr.offsets, r(fr.opaque_depth),
+                              r(fr.opaque_color))
+
+    cases = {
+        "ragged": synth_to_reference(synth.generate("ragged", 16, 12, seed=3, layers=40)),
+        "particles": synth_to_reference(synth.generate("particles", 8, 6, seed=9, layers=64)),
+        "smokefire_shuf": f32_frame(cast_frame(preset("smoke-fire"), 24, 24).shuffled(7)),
+        "wine": f32_frame(cast_frame(preset("wine-bottle"), 33, 33)),
+    }
+    out = {}
+    for name, fr in cases.items():
+        bg = fr.opaque_color
+        near = np.full(fr.npix, np.inf)
+        far = np.full(fr.npix, -np.inf)
+        np.minimum.at(near, fr.pixel, fr.depth)
+        np.maximum.at(far, fr.pixel, fr.depth)
+        for cube in (False, True):
+            tag = f"{name}_{'cube' if cube else 'plain'}"
+            out[f"abuffer_{tag}"] = rb.abuffer_frame(fr, bg, cube)
+            out[f"wboit_{tag}"] = rb.wboit_frame(fr, bg, near, far, cube, rb.DEFAULT_WBOIT_WEIGHT)
+            out[f"mlab4_{tag}"] = rb.mlab_frame(fr, bg, 4, cube)
+        if name in ("smokefire_shuf", "wine"):
+            f32 = lambda a: np.asarray(a, dtype=np.float32)
+            out[f"in_{name}"] = np.array(repr(dict(width=fr.width, height=fr.height)))
+            for k in ("offsets", "depth", "alpha", "trans", "radiance", "normal", "ior", "backface",
+                      "opaque_depth", "opaque_color"):
+                a = getattr(fr, k)
+                out[f"in_{name}_{k}"] = a if k in ("offsets", "backface") else f32(a)
+    save("baselines", **out)
+
+
 def main():
+    if "--only-baselines" in sys.argv:
+        baselines_case()
+        return
     # config 1 of BASELINE.json: 64x64, the single-plane pane + 4 random layers, rank 3
     synth_case("plane4_64", "plane4", 64, 64, 1, 5, rank=3)
     # ragged CSR (empty pixels, runs up to 40) at every supported rank
@@ -170,6 +213,7 @@ def main():
     scene_case("single5_r3", "single-plane", 5, 5, rank=3)
     scene_case("glass9_packed", "glass-stack", 9, 9, rank=3, packed_storage=True)
     kernel_case()
+    baselines_case()
 
 
 if __name__ == "__main__":

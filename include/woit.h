@@ -172,6 +172,61 @@ int woit_build_atomic(const woit_frags_t* frags, const int32_t* pix, const woit_
 int woit_fragment_indices(const woit_frags_t* frags, const float* near, const float* far, int rank,
                           double* z, int32_t* slots, int32_t* cells, void* stream);
 
+/* ---- on-device fragment producer (scene.py:430-630 cast_frame) ---------------
+ * Casts every pixel's primary ray against an analytic scene and writes the CSR
+ * stream (fp32, the layout above) in cast_frame's row order: per pixel, primitives
+ * in scene order, sub-index order inside a primitive (sphere entry then exit, fog
+ * slices front to back, particles by index). Geometry in float64. */
+#define WOIT_PRIM_PLANE 0
+#define WOIT_PRIM_SPHERE 1
+#define WOIT_PRIM_FOG 2
+#define WOIT_PRIM_PARTICLES 3
+#define WOIT_PRIM_BACKDROP 4
+
+typedef struct woit_prim {
+    int32_t kind;           /* WOIT_PRIM_* */
+    int32_t count;          /* fog: slices; particles: particle count */
+    int32_t profile;        /* particles: 0 gauss, 1 mask */
+    int32_t flags;          /* bit 0: plane has an extent (pane); bit 1: backdrop checker */
+    double d;               /* plane / backdrop forward distance */
+    double center[3];       /* sphere / particle-cloud centre */
+    double radius;          /* sphere radius */
+    double particle_radius; /* particle disc radius */
+    double extent[2];       /* pane half extents */
+    double pcenter[2];      /* pane centre (right, up) */
+    double alpha, ior;      /* material */
+    double trans[3], radiance[3];
+    double sigma[3];        /* fog extinction */
+    double color[3];        /* fog in-scatter colour; backdrop colour */
+    double checker[3];      /* backdrop checker colour */
+    double near, far;       /* fog slab */
+    double cell;            /* backdrop checker cell (world units) */
+    const double* positions;      /* particles: device [count][3] */
+    const double* radiance_scale; /* particles: device [count] */
+    const int32_t* box;           /* particles: device [count][4] screen box x0, x1, y0, y1
+                                     (cast_frame's conservative bound; x0 > x1 = culled) */
+} woit_prim_t;
+
+typedef struct woit_scene {
+    int32_t nprims;
+    int32_t bg_cell;          /* background checker cell in pixels */
+    int32_t bg_has_checker;
+    int32_t reserved;
+    const woit_prim_t* prims; /* DEVICE array [nprims] */
+    double origin[3], forward[3], right[3], up[3];  /* Camera.basis() */
+    double tan_half, aspect;
+    double bg_color[3], bg_checker[3];
+} woit_scene_t;
+
+size_t woit_cast_workspace_bytes(int64_t npix);
+/* offsets[W*H+1] of the frame's CSR stream (pass 1). */
+int woit_cast_offsets(const woit_scene_t* scene, int32_t width, int32_t height, int64_t* offsets, void* ws,
+                      size_t ws_bytes, void* stream);
+/* the fragment arrays (sized by offsets[W*H]) and the opaque depth / colour (pass 2). */
+int woit_cast_fill(const woit_scene_t* scene, int32_t width, int32_t height, const int64_t* offsets,
+                   float* depth, float* alpha, float* trans, float* radiance, float* normal, float* ior,
+                   uint8_t* backface, float* opaque_depth, float* opaque_color, void* stream);
+
 /* ---- comparison methods (RenderConfig.method, baselines.py:135-220) ---------
  * The reference's non-wavelet methods over the same CSR stream, in float64 with the
  * reference's operation order (one thread per pixel), output fp32 [npix][3] over the

@@ -19,3 +19,4 @@ from .pipeline import (METHODS, Camera, FrameBuffers, RayGrid, RenderConfig, Wor
 from .packing import pack_rgb9e5, unpack_rgb9e5, roundtrip_coeff_array, bytes_per_pixel  # noqa: F401
 
 __version__ = "0.1.0"
+from .scene import PRESET_NAMES, Scene, cast_frame, preset  # noqa: F401,E402

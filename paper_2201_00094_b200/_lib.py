@@ -64,6 +64,28 @@ class Bufs(C.Structure):
                 ("full_opaque_image", _vp), ("diffusion", _vp), ("blurred_image", _vp)]
 
 
+_d3 = C.c_double * 3
+_d2 = C.c_double * 2
+
+
+class Prim(C.Structure):
+    """woit_prim_t"""
+    _fields_ = [("kind", _i32), ("count", _i32), ("profile", _i32), ("flags", _i32), ("d", C.c_double),
+                ("center", _d3), ("radius", C.c_double), ("particle_radius", C.c_double), ("extent", _d2),
+                ("pcenter", _d2), ("alpha", C.c_double), ("ior", C.c_double), ("trans", _d3), ("radiance", _d3),
+                ("sigma", _d3), ("color", _d3), ("checker", _d3), ("near", C.c_double), ("far", C.c_double),
+                ("cell", C.c_double), ("positions", _vp), ("radiance_scale", _vp), ("box", _vp)]
+
+
+class SceneC(C.Structure):
+    """woit_scene_t"""
+    _fields_ = [("nprims", _i32), ("bg_cell", _i32), ("bg_has_checker", _i32), ("reserved", _i32), ("prims", _vp),
+                ("origin", _d3), ("forward", _d3), ("right", _d3), ("up", _d3), ("tan_half", C.c_double),
+                ("aspect", C.c_double), ("bg_color", _d3), ("bg_checker", _d3)]
+
+
+PRIM_PLANE, PRIM_SPHERE, PRIM_FOG, PRIM_PARTICLES, PRIM_BACKDROP = 0, 1, 2, 3, 4
+
 _SIGS = {
     "woit_abi_version": (C.c_int, []),
     "woit_status_string": (C.c_char_p, [C.c_int]),
@@ -78,6 +100,10 @@ _SIGS = {
     "woit_blur_workspace_bytes": (_sz, [_i32, _i32]),
     "woit_build_atomic_workspace_bytes": (_sz, [_i64]),
     "woit_baseline_workspace_bytes": (_sz, [C.c_int, _i64, _i64]),
+    "woit_cast_workspace_bytes": (_sz, [_i64]),
+    "woit_cast_offsets": (C.c_int, [C.POINTER(SceneC), _i32, _i32, _vp, _vp, _sz, _vp]),
+    "woit_cast_fill": (C.c_int, [C.POINTER(SceneC), _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                 _vp]),
     "woit_render_baseline": (C.c_int, [C.POINTER(Frags), C.c_int, C.c_int, _vp, _vp, _vp, _sz, _vp]),
     "woit_build_atomic": (C.c_int, [C.POINTER(Frags), _vp, C.POINTER(Params), C.POINTER(Bufs), _vp, _sz, _vp]),
     "woit_resolve_blur": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _vp, _sz, _vp]),

@@ -192,6 +192,36 @@ int woit_fragment_indices(const woit_frags_t* frags, const float* near, const fl
     return cuda_status(launch_indices(kp, z, slots, cells, static_cast<cudaStream_t>(stream)));
 }
 
+size_t woit_cast_workspace_bytes(int64_t npix) { return npix < 0 ? 0 : cast_workspace(npix); }
+
+static int check_scene(const woit_scene_t* s, int32_t W, int32_t H) {
+    if (!s || W < 1 || H < 1 || s->nprims < 0 || (s->nprims > 0 && !s->prims)) return WOIT_EINVAL;
+    if (s->bg_has_checker && s->bg_cell < 1) return WOIT_EINVAL;
+    if ((int64_t)W * H >= ((int64_t)1 << 31)) return WOIT_EINVAL;  // CUB scan item count
+    return WOIT_OK;
+}
+
+int woit_cast_offsets(const woit_scene_t* scene, int32_t width, int32_t height, int64_t* offsets, void* ws,
+                      size_t ws_bytes, void* stream) {
+    int s = check_scene(scene, width, height);
+    if (s) return s;
+    if (!offsets) return WOIT_EINVAL;
+    if (!ws || ws_bytes < cast_workspace((int64_t)width * height)) return WOIT_EWORKSPACE;
+    return cuda_status(cast_count(*scene, width, height, offsets, ws, static_cast<cudaStream_t>(stream)));
+}
+
+int woit_cast_fill(const woit_scene_t* scene, int32_t width, int32_t height, const int64_t* offsets, float* depth,
+                   float* alpha, float* trans, float* radiance, float* normal, float* ior, uint8_t* backface,
+                   float* opaque_depth, float* opaque_color, void* stream) {
+    int s = check_scene(scene, width, height);
+    if (s) return s;
+    if (!offsets || !depth || !alpha || !trans || !radiance || !normal || !ior || !backface || !opaque_depth ||
+        !opaque_color)
+        return WOIT_EINVAL;
+    return cuda_status(cast_fill(*scene, width, height, offsets, depth, alpha, trans, radiance, normal, ior, backface,
+                                 opaque_depth, opaque_color, static_cast<cudaStream_t>(stream)));
+}
+
 size_t woit_baseline_workspace_bytes(int method, int64_t npix, int64_t nfrag) {
     if (method < WOIT_METHOD_ABUFFER || method > WOIT_METHOD_MLAB4 || npix < 0 || nfrag < 0) return 0;
     return baseline_workspace(method, npix, nfrag);

@@ -24,6 +24,11 @@ cudaError_t unpack(const uint32_t* words, int64_t n, double* out, cudaStream_t s
 size_t blur_workspace(int32_t width, int32_t height);
 size_t build_atomic_workspace(int64_t npix);
 size_t baseline_workspace(int method, int64_t npix, int64_t nfrag);
+size_t cast_workspace(int64_t npix);
+cudaError_t cast_count(const woit_scene_t& s, int W, int H, int64_t* offsets, void* ws, cudaStream_t st);
+cudaError_t cast_fill(const woit_scene_t& s, int W, int H, const int64_t* offsets, float* depth, float* alpha,
+                      float* trans, float* rad, float* normal, float* ior, uint8_t* bf, float* od, float* oc,
+                      cudaStream_t st);
 cudaError_t render_baseline(const woit_frags_t& f, int method, bool cube, const double wboit[3], float* out,
                             void* ws, cudaStream_t st);
 cudaError_t build_atomic(const int32_t* pix, const woit_frags_t& f, int rank, int flags, const float* near,

@@ -11,8 +11,8 @@ fragment from HBM once.
 Differences from the reference, all deliberate:
 * fp32 storage (the reference is float64); z and every index derived from it
   are still computed in f64 / fixed point and are bit-identical;
-* ``render_frame`` needs ``frame=``: the analytic caster (scene.py:463-630) is
-  out of scope, so there is no scene -> fragments step here;
+* without ``frame=``, ``render_frame`` casts the scene on the GPU
+  (``scene.cast_frame``, the reference's scene.py:463-630);
 * the comparison methods (``method="abuffer" | "wboit" | "mlab4"``,
   baselines.py:135-220) run as float64 per-pixel kernels (``render_baseline``);
   they need ``frame=`` like the wavelet path;
@@ -412,7 +412,12 @@ def render_frame(scene, cfg: RenderConfig, counter: Optional[TouchCounter] = Non
     one after another; the result is bit-identical to one band.
     """
     if frame is None:
-        raise NotImplementedError("scene casting (scene.py:463-630) is out of scope: pass frame=")
+        # cast on the device (scene.py:463-630 -> paper_2201_00094_b200.scene.cast_frame)
+        from .scene import Scene, cast_frame
+
+        if not isinstance(scene, Scene):
+            raise ValueError("render_frame without frame= needs a Scene to cast")
+        frame = cast_frame(scene, cfg.width, cfg.height)
     if frame.npix != cfg.width * cfg.height:
         raise ValueError("frame size does not match the config")
     if cfg.method != "wavelet":

@@ -16,7 +16,7 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 def names():
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
-                  if not p.endswith(("kernels.npz", "baselines.npz")))
+                  if not p.endswith(("kernels.npz", "baselines.npz", "cast.npz")))
 
 
 def load(name: str):

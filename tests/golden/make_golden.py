@@ -183,9 +183,43 @@ def baselines_case():
     save("baselines", **out)
 
 
+def cast_case():
+    """The reference caster's CSR output (scene.py:463-630) for every preset at 32x24 and
+    for test_scene.py's wide-fov corner-particle scene, plus the seeded particle
+    positions (pins the scene description the device caster restates)."""
+    from woit.scene import Material, OpaqueBackdrop, ParticleCloud
+    from woit.core import Spectrum3
+
+    mat = Material(alpha=0.6, transmission=Spectrum3.gray(0.2), radiance=Spectrum3.gray(0.4))
+    wide = Scene(Camera(fov_deg=95.0),
+                 (ParticleCloud(center=(-1.9, 0.9, 1.2), radius=0.5, count=60, particle_radius=0.2, material=mat,
+                                seed_offset=1),
+                  ParticleCloud(center=(2.1, -1.0, 1.4), radius=0.6, count=60, particle_radius=0.25, material=mat,
+                                profile="mask", seed_offset=2),
+                  OpaqueBackdrop(d=4.0, color=Spectrum3.gray(0.5))), rng_seed=3)
+    from woit.scene import PRESET_NAMES
+    scenes = [(n, preset(n), 32, 24) for n in PRESET_NAMES] + [("wide-fov", wide, 48, 20)]
+    out = {}
+    for name, sc, W, H in scenes:
+        fr = cast_frame(sc, W, H)
+        key = name.replace("-", "_")
+        out[f"{key}_size"] = np.array([W, H])
+        for k in ("offsets", "depth", "alpha", "trans", "radiance", "normal", "ior", "backface", "opaque_depth",
+                  "opaque_color"):
+            out[f"{key}_{k}"] = getattr(fr, k)
+        for j, pr in enumerate(sc.primitives):
+            if isinstance(pr, ParticleCloud):
+                out[f"{key}_p{j}_positions"] = pr.positions
+                out[f"{key}_p{j}_scale"] = pr.radiance_scale
+    save("cast", **out)
+
+
 def main():
     if "--only-baselines" in sys.argv:
         baselines_case()
+        return
+    if "--only-cast" in sys.argv:
+        cast_case()
         return
     # config 1 of BASELINE.json: 64x64, the single-plane pane + 4 random layers, rank 3
     synth_case("plane4_64", "plane4", 64, 64, 1, 5, rank=3)
@@ -214,6 +248,7 @@ def main():
     scene_case("glass9_packed", "glass-stack", 9, 9, rank=3, packed_storage=True)
     kernel_case()
     baselines_case()
+    cast_case()
 
 
 if __name__ == "__main__":

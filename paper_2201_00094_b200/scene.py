@@ -195,6 +195,93 @@ def preset(name: str) -> Scene:
 
 
 # ---------------------------------------------------------------------------
+# scene description files (the grammar of scene.py:1-26, parse_scene :783-850)
+
+
+def _floats(text: str, n: int) -> Tuple[float, ...]:
+    parts = text.split(",")
+    if len(parts) != n:
+        raise ValueError(f"expected {n} comma-separated numbers, got {text!r}")
+    return tuple(float(p) for p in parts)
+
+
+def _material(kv) -> Material:
+    return Material(float(kv.pop("alpha", 1.0)), _floats(kv.pop("transmission", "1,1,1"), 3),
+                    _floats(kv.pop("radiance", "0,0,0"), 3), float(kv.pop("ior", 1.0)))
+
+
+def parse_scene(text: str) -> Scene:
+    camera, background, seed, prims = Camera(), Background(), 0, []
+    for line_no, raw in enumerate(text.splitlines(), start=1):
+        line = raw.split("#", 1)[0].strip()
+        if not line:
+            continue
+        head, *rest = line.split()
+        if head == "seed":
+            if len(rest) != 1:
+                raise ValueError(f"line {line_no}: seed takes one integer")
+            seed = int(rest[0])
+            continue
+        kv = {}
+        for tok in rest:
+            if "=" not in tok:
+                raise ValueError(f"line {line_no}: expected key=value, got {tok!r}")
+            k, v = tok.split("=", 1)
+            kv[k] = v
+        try:
+            if head == "camera":
+                camera = Camera(_floats(kv.pop("pos", "0,0,0"), 3), _floats(kv.pop("forward", "0,0,1"), 3),
+                                float(kv.pop("fov", 60.0)))
+            elif head == "background":
+                checker = kv.pop("checker", None)
+                background = Background(_floats(kv.pop("color", "0.05,0.06,0.08"), 3),
+                                        _floats(checker, 3) if checker else None, int(kv.pop("cell", 16)))
+            elif head == "plane":
+                d = float(kv.pop("d"))
+                extent = kv.pop("extent", None)
+                center = kv.pop("center", "0,0")
+                prims.append(Plane(d, _material(kv), _floats(extent, 2) if extent else None, _floats(center, 2)))
+            elif head == "sphere":
+                center = _floats(kv.pop("center"), 3)
+                radius = float(kv.pop("radius"))
+                prims.append(Sphere(center, radius, _material(kv)))
+            elif head == "fog_slab":
+                prims.append(FogSlab(float(kv.pop("near")), float(kv.pop("far")), _floats(kv.pop("sigma"), 3),
+                                     int(kv.pop("slices", 32)), _floats(kv.pop("color", "0,0,0"), 3)))
+            elif head == "particle_cloud":
+                center = _floats(kv.pop("center"), 3)
+                radius = float(kv.pop("radius"))
+                count = int(kv.pop("count"))
+                pr = float(kv.pop("particle_radius"))
+                profile = kv.pop("profile", "gauss")
+                seed_offset = int(kv.pop("seed_offset", 0))
+                prims.append(ParticleCloud(center, radius, count, pr, _material(kv), profile, seed_offset))
+            elif head == "opaque_backdrop":
+                checker = kv.pop("checker", None)
+                prims.append(OpaqueBackdrop(float(kv.pop("d")), _floats(kv.pop("color"), 3),
+                                            _floats(checker, 3) if checker else None, float(kv.pop("cell", 0.5))))
+            else:
+                raise ValueError(f"unknown primitive {head!r}")
+        except KeyError as exc:
+            raise ValueError(f"line {line_no}: {head} is missing required key {exc}") from None
+        if kv:
+            raise ValueError(f"line {line_no}: unknown keys for {head}: {', '.join(sorted(kv))}")
+    return Scene(camera, tuple(prims), background, seed)
+
+
+def load_scene(path) -> Scene:
+    with open(path, "r", encoding="utf-8") as fh:
+        return parse_scene(fh.read())
+
+
+def resolve_scene(name_or_path: str) -> Scene:
+    """Preset name, or path to a scene description file."""
+    import os
+
+    return load_scene(name_or_path) if os.path.exists(name_or_path) else preset(name_or_path)
+
+
+# ---------------------------------------------------------------------------
 # device scene + caster
 
 

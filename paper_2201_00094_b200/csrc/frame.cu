@@ -31,6 +31,12 @@
 #ifndef WOIT_DYN  // dynamic window claims
 #define WOIT_DYN 1
 #endif
+#ifndef WOIT_EVPIPE  // software-pipelined evaluation loop
+#define WOIT_EVPIPE 1
+#endif
+#ifndef WOIT_BPIPE
+#define WOIT_BPIPE 0
+#endif
 #ifndef WOIT_FFMA2
 #define WOIT_FFMA2 1
 #endif
@@ -146,17 +152,16 @@ WOIT_D void store_cells(float2* cells, int kq, int kch, const TV v[M]) {
 // Fast-path chunk loops as functions with __restrict__ parameters: the compiler may
 // then move the loads of later fragments above the shared-memory stores of earlier
 // ones (the pointers provably do not alias), which it cannot do in the kernel body.
+// Fragment part of the build: z (fused; stored for the evaluation over the staged
+// depth), opacity alpha (1 - T) (stored in the T slot for the evaluation) and the
+// absorbance a = -ln(max(1e-6, 1 - opacity)) per channel.
 template <int R>
-WOIT_D void build_frag(zfix_t* WOIT_ZR zf, const float* WOIT_ZR dep, const DepthMap& m,
-                       const float* __restrict__ alp, float* __restrict__ trs, float* __restrict__ part,
-                       float* __restrict__ sink, int lane, int fr, int si) {
-    constexpr int M = 2 << R, WC = 32;
-    // z fused into the build and stored for the evaluation (fast path: in place of
-    // the depth, which nothing reads afterwards)
-    const zfix_t zi = z_fixed_of(dep[si], m);
+WOIT_D void build_prep(zfix_t* WOIT_ZR zf, const float* WOIT_ZR dep, const DepthMap& m,
+                       const float* __restrict__ alp, float* __restrict__ trs, int fr, int si, zfix_t& zi,
+                       float a[3]) {
+    zi = z_fixed_of(dep[si], m);
     zf[fr] = zi;
     const float al = alp[si];
-    float a[3];
 #if WOIT_FFMA2
     {   // channels 0 and 1 paired (bit-identical to the scalar sequence), channel 2 scalar
         const float2 one = make_float2(1.0f, 1.0f);
@@ -181,6 +186,12 @@ WOIT_D void build_frag(zfix_t* WOIT_ZR zf, const float* WOIT_ZR dep, const Depth
         a[ch] = -log_poly(fmaxf((float)kTransFloor, 1.0f - op));
     }
 #endif
+}
+
+// Difference-array part: a (1 - w) to D_j, a w to D_{j+1} of this lane's partials.
+template <int R>
+WOIT_D void build_accum(float* __restrict__ part, float* __restrict__ sink, int lane, zfix_t zi, const float a[3]) {
+    constexpr int M = 2 << R, WC = 32;
     const int cell = (int)(zi >> (kZBits - (R + 1)));
     const float fr_ = u32_to_unit(zi << (R + 1), kZBits);  // M z - j_f
     float* d = part + cell * 3 * WC + lane;
@@ -194,18 +205,42 @@ WOIT_D void build_frag(zfix_t* WOIT_ZR zf, const float* WOIT_ZR dep, const Depth
 }
 
 // The chunk loops visit fragment (crot + j) mod clen at step j. (Fully unrolled
-// loops for full chunks measured 3.5% slower: code size.)
+// loops for full chunks measured 3.5% slower: code size. Software pipelining of
+// this loop -- the next fragment's prep beside this one's updates, WOIT_BPIPE --
+// measured 4% slower; the evaluation loop's pipelining pays.)
 template <int R>
 WOIT_D void build_chunk_fast(zfix_t* WOIT_ZR zf, const float* WOIT_ZR dep, const DepthMap m,
                              const float* __restrict__ alp, float* __restrict__ trs, float* __restrict__ part,
                              float* __restrict__ sink, int lane, int cst, int clen, int crot, int sh4) {
+#if WOIT_BPIPE
+    if (clen <= 0) return;
+    int jj = crot;
+    zfix_t zi;
+    float a[3];
+    build_prep<R>(zf, dep, m, alp, trs, cst + jj, sh4 + cst + jj, zi, a);
+#pragma unroll 1
+    for (int j = 0; j < clen; ++j) {
+        jj = jj + 1 == clen ? 0 : jj + 1;
+        zfix_t zn = 0;
+        float an[3] = {0.0f, 0.0f, 0.0f};
+        if (j + 1 < clen) build_prep<R>(zf, dep, m, alp, trs, cst + jj, sh4 + cst + jj, zn, an);
+        build_accum<R>(part, sink, lane, zi, a);
+        zi = zn;
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) a[ch] = an[ch];
+    }
+#else
     int jj = crot;
 #pragma unroll kUnroll
     for (int j = 0; j < clen; ++j) {
         const int fr = cst + jj;
         jj = jj + 1 == clen ? 0 : jj + 1;
-        build_frag<R>(zf, dep, m, alp, trs, part, sink, lane, fr, sh4 + fr);
+        zfix_t zi;
+        float a[3];
+        build_prep<R>(zf, dep, m, alp, trs, fr, sh4 + fr, zi, a);
+        build_accum<R>(part, sink, lane, zi, a);
     }
+#endif
 }
 
 template <int R>
@@ -233,6 +268,60 @@ WOIT_D void eval_chunk_fast(const zfix_t* __restrict__ zf, const float* __restri
                             const float* __restrict__ opw, const float2* __restrict__ cq2,
                             float* __restrict__ rad, int cst, int clen, int crot, int sh4, float ac[3],
                             float wg[3]) {
+#if WOIT_EVPIPE
+    // software-pipelined: the next fragment's scalar operands are loaded before
+    // this fragment's v̂ stores (different fragments, so no hazard; the wrap-around
+    // prefetch after the last fragment is discarded)
+    if (clen <= 0) return;
+    int jj = crot;
+    int fr = cst + jj;
+    zfix_t z = zf[fr];
+    float al = alp[sh4 + fr];
+    float L[3], op[3];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        L[ch] = rad[3 * (sh4 + fr) + ch];
+        op[ch] = opw[3 * (sh4 + fr) + ch];
+    }
+#pragma unroll 1
+    for (int j = 0; j < clen; ++j) {
+        const int si = sh4 + fr;
+        int c0;
+        float t;
+        eval_cell(z, R, c0, t);
+        const float2* cv = cq2 + c0 * 3;
+        float2 vd[3];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) vd[ch] = cv[ch];
+        const int jn = jj + 1 == clen ? 0 : jj + 1;
+        const int frn = cst + jn, sin = sh4 + frn;
+        const zfix_t zn = zf[frn];
+        const float aln = alp[sin];
+        float Ln[3], opn[3];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            Ln[ch] = rad[3 * sin + ch];
+            opn[ch] = opw[3 * sin + ch];
+        }
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            const float A = fmaxf(fmaf(t, vd[ch].y, vd[ch].x), 0.0f);
+            const float vh = exp_neg(A);
+            ac[ch] += (L[ch] * al) * vh;
+            wg[ch] += op[ch] * vh;
+            rad[3 * si + ch] = vh;  // v̂ replaces radiance in place
+        }
+        jj = jn;
+        fr = frn;
+        z = zn;
+        al = aln;
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            L[ch] = Ln[ch];
+            op[ch] = opn[ch];
+        }
+    }
+#else
     int jj = crot;
 #pragma unroll kUnroll
     for (int j = 0; j < clen; ++j) {
@@ -240,6 +329,7 @@ WOIT_D void eval_chunk_fast(const zfix_t* __restrict__ zf, const float* __restri
         jj = jj + 1 == clen ? 0 : jj + 1;
         eval_frag<R>(zf, alp, opw, cq2, rad, fr, sh4 + fr, ac, wg);
     }
+#endif
 }
 
 // ---------------------------------------------------------------------------

@@ -269,39 +269,41 @@ WOIT_D void eval_chunk_fast(const zfix_t* __restrict__ zf, const float* __restri
                             float* __restrict__ rad, int cst, int clen, int crot, int sh4, float ac[3],
                             float wg[3]) {
 #if WOIT_EVPIPE
-    // software-pipelined: the next fragment's scalar operands are loaded before
-    // this fragment's v̂ stores (different fragments, so no hazard; the wrap-around
-    // prefetch after the last fragment is discarded)
+    // software-pipelined: the next fragment's operands -- and, at depth 2, its cell
+    // pair -- are loaded before this fragment's v̂ stores (different fragments, so
+    // no hazard; the wrap-around prefetch after the last fragment is discarded)
     if (clen <= 0) return;
     int jj = crot;
     int fr = cst + jj;
-    zfix_t z = zf[fr];
     float al = alp[sh4 + fr];
     float L[3], op[3];
+    float2 vd[3];
+    float t;
+    {
+        int c0;
+        eval_cell(zf[fr], R, c0, t);
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-        L[ch] = rad[3 * (sh4 + fr) + ch];
-        op[ch] = opw[3 * (sh4 + fr) + ch];
+        for (int ch = 0; ch < 3; ++ch) {
+            L[ch] = rad[3 * (sh4 + fr) + ch];
+            op[ch] = opw[3 * (sh4 + fr) + ch];
+            vd[ch] = cq2[c0 * 3 + ch];
+        }
     }
 #pragma unroll 1
     for (int j = 0; j < clen; ++j) {
         const int si = sh4 + fr;
-        int c0;
-        float t;
-        eval_cell(z, R, c0, t);
-        const float2* cv = cq2 + c0 * 3;
-        float2 vd[3];
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) vd[ch] = cv[ch];
         const int jn = jj + 1 == clen ? 0 : jj + 1;
         const int frn = cst + jn, sin = sh4 + frn;
-        const zfix_t zn = zf[frn];
         const float aln = alp[sin];
-        float Ln[3], opn[3];
+        float Ln[3], opn[3], tn;
+        float2 vdn[3];
+        int cn;
+        eval_cell(zf[frn], R, cn, tn);
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
             Ln[ch] = rad[3 * sin + ch];
             opn[ch] = opw[3 * sin + ch];
+            vdn[ch] = cq2[cn * 3 + ch];
         }
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
@@ -313,12 +315,13 @@ WOIT_D void eval_chunk_fast(const zfix_t* __restrict__ zf, const float* __restri
         }
         jj = jn;
         fr = frn;
-        z = zn;
         al = aln;
+        t = tn;
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
             L[ch] = Ln[ch];
             op[ch] = opn[ch];
+            vd[ch] = vdn[ch];
         }
     }
 #else

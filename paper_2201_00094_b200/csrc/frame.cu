@@ -493,8 +493,61 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
         if (win * WIN + lane < end) off_lane = kp.f.offsets[win * WIN + lane];
         off_last = kp.f.offsets[end];
     }
+    // Fast path: a sub-tile's composite (phase 7) is deferred until the next
+    // sub-tile's staging copies are in flight, so it hides part of their latency.
+    // It only reads the per-window chunk prefix, the chunk accumulators, v_tot and
+    // the staged opaque colours (taken into a register before the next copies).
+    bool pend = false;
+    int pq0 = 0, pnqs = 0;
+    int64_t pw0 = 0;
+    auto composite_fast = [&](int cq0, int cnqs, int64_t cw0, float bgr) {
+        if (lane >= 3 * cnqs) return;
+        const int kch = lane / cnqs, kq = lane - kch * cnqs;
+        const int q = cq0 + kq;
+        const int64_t p = cw0 + q;
+        const int nc = (sm.cb[q + 1] - sm.cb[q]);
+        const int cbq = sm.cb[q] - sm.cb[cq0];
+        double acc = 0.0, wgt = 0.0;
+        for (int i = 0; i < nc; ++i) {
+            acc += (double)sm.accp[kch * WC + cbq + i];
+            wgt += (double)sm.accp[(3 + kch) * WC + cbq + i];
+        }
+        if (kp.b.accum) kp.b.accum[p * 3 + kch] = (float)acc;
+        if (kp.b.weight) kp.b.weight[p * 3 + kch] = (float)wgt;
+        if (kp.b.output) {
+            const double bg = (double)bgr;
+            const double vt = sm.vtot[kq * 3 + kch];
+            double o;
+            if (flags & WOIT_NORMALIZE) {
+                const double avg = acc * rcp_refined(fmax(kNormEps, wgt));
+                o = dadd(dmul(avg, 1.0 - vt), dmul(bg, vt));
+            } else {
+                o = dadd(acc, dmul(bg, vt));
+            }
+            kp.b.output[p * 3 + kch] = (float)o;
+        }
+        if (kch == 0 && kp.b.refraction_offset) {
+            kp.b.refraction_offset[p * 2] = 0.0f;
+            kp.b.refraction_offset[p * 2 + 1] = 0.0f;
+        }
+    };
+    // this lane's opaque colour of the pending composite, from the staged copy
+    auto pending_bg = [&]() -> float {
+        if (!pend || lane >= 3 * pnqs || !kp.b.output) return 0.0f;
+        const int kch = lane / pnqs, kq = lane - kch * pnqs;
+        const int si = (int)(pw0 + pq0 + kq - ((pw0 + pq0) & ~(int64_t)3));
+        return sm.opq[3 * si + kch];
+    };
+    auto flush = [&]() {
+        if (!GEN && pend) {
+            composite_fast(pq0, pnqs, pw0, pending_bg());
+            pend = false;
+            __syncwarp();
+        }
+    };
     int64_t next_win = nwin;
     for (; win < nwin; win = next_win) {
+    flush();  // the pending composite reads this window's chunk prefix
     const int64_t w0 = win * WIN;
     const int nq = (int)((kp.f.npix - w0) < WIN ? (kp.f.npix - w0) : WIN);
     if (lane < nq) sm.offs[lane] = off_lane;
@@ -565,6 +618,11 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
         const int sh4 = (int)(fa - a4);  // staging index of fragment fa (granule-4 arrays)
         const int shb = (int)(fa - a16);
 
+        // the previous sub-tile's deferred composite: its opaque colours out of the
+        // staging buffer before this sub-tile's copies overwrite it
+        const float pbg = GEN ? 0.0f : pending_bg();
+        if (!GEN) __syncwarp();
+
         // ---- 1. stage fragment fields (TMA bulk copies, one mbarrier per warp) ----
         // All 4-byte-element and 12-byte-element arrays share the 16-B granule
         // window [a4, b4): one bulk copy each; lanes load the < 4-fragment tail
@@ -634,6 +692,12 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
                 for (int i = lane; i < (int)(fb - fa); i += 32) sm.ior[sh4 + i] = 1.0f;
             if (GEN && bfonly && !kp.f.backface)
                 for (int i = lane; i < (int)(fb - fa); i += 32) sm.bf[shb + i] = 0;
+        }
+
+        if (!GEN && pend) {  // overlaps the copies just issued
+            composite_fast(pq0, pnqs, pw0, pbg);
+            pend = false;
+            __syncwarp();
         }
 
         // ---- 2. chunk table + per-pixel init (overlaps the copies) -----------------
@@ -999,38 +1063,11 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
 
         // ---- 7. per-pixel accumulators + composite (step4) -------------------------
         if (!GEN) {
-            // fast path: one lane per (pixel, channel) -- the channels are independent
-            if (lane < 3 * nqs) {
-                const int kch = lane / nqs, kq = lane - kch * nqs;
-                const int q = q0 + kq;
-                const int64_t p = w0 + q;
-                const int nc = (sm.cb[q + 1] - sm.cb[q]);
-                const int cbq = sm.cb[q] - sm.cb[q0];
-                double acc = 0.0, wgt = 0.0;
-                for (int i = 0; i < nc; ++i) {
-                    acc += (double)sm.accp[kch * WC + cbq + i];
-                    wgt += (double)sm.accp[(3 + kch) * WC + cbq + i];
-                }
-                if (kp.b.accum) kp.b.accum[p * 3 + kch] = (float)acc;
-                if (kp.b.weight) kp.b.weight[p * 3 + kch] = (float)wgt;
-                if (kp.b.output) {
-                    const int si = (int)(p - ((w0 + q0) & ~(int64_t)3));
-                    const double bg = (double)sm.opq[3 * si + kch];
-                    const double vt = sm.vtot[kq * 3 + kch];
-                    double o;
-                    if (flags & WOIT_NORMALIZE) {
-                        const double avg = acc * rcp_refined(fmax(kNormEps, wgt));
-                        o = dadd(dmul(avg, 1.0 - vt), dmul(bg, vt));
-                    } else {
-                        o = dadd(acc, dmul(bg, vt));
-                    }
-                    kp.b.output[p * 3 + kch] = (float)o;
-                }
-                if (kch == 0 && kp.b.refraction_offset) {
-                    kp.b.refraction_offset[p * 2] = 0.0f;
-                    kp.b.refraction_offset[p * 2 + 1] = 0.0f;
-                }
-            }
+            // fast path: deferred to the next sub-tile's staging (composite_fast)
+            pend = true;
+            pq0 = q0;
+            pnqs = nqs;
+            pw0 = w0;
         } else if (lane < 3 * nqs) {
             // general path: one lane per (pixel, channel) as well; the refraction and
             // diffusion sums are per pixel, and every channel lane forms them in the
@@ -1081,6 +1118,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
         q0 = q1;
     }
     }  // window loop
+    flush();
     if (lane == 0) bulk_wait_all();
 }
 

@@ -64,7 +64,10 @@ WOIT_D void unpack_chunk(uint32_t c, int& q, int& start, int& len) {
 // fragment id of the chunk start: it spreads the lanes of a warp over the 32
 // smem banks for uniform run lengths and keeps the summation order independent
 // of the tiling (bit-identical results for any band split).
-WOIT_D int chunk_rotation(int64_t gstart, int len) { return (int)((uint32_t)(gstart >> 5) % (uint32_t)len); }
+WOIT_D int chunk_rotation(int64_t gstart, int len) {
+    const uint32_t g = (uint32_t)(gstart >> 5);
+    return (int)(len == 8 ? (g & 7u) : g % (uint32_t)len);  // full chunks: no division
+}
 
 
 // ---------------------------------------------------------------------------
@@ -735,12 +738,21 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
         if (ph & PH_BOUNDS) {
             if (lane < C) {
                 float mn = INFINITY, mx = -INFINITY;
-                int jj = crot;  // rotated start: conflict-free banks across lanes
-                for (int j = 0; j < clen; ++j) {
-                    const float x = sm.depth[sh4 + cst + jj];
-                    jj = jj + 1 == clen ? 0 : jj + 1;
-                    mn = fminf(mn, x);
-                    mx = fmaxf(mx, x);
+                if (clen == CH && ((sh4 + cst) & 3) == 0) {
+                    // min / max do not depend on the order: two 16-B loads per full chunk,
+                    // the halves swapped on odd lanes to spread the banks
+                    const float4* d4 = reinterpret_cast<const float4*>(sm.depth + sh4 + cst);
+                    const float4 u = d4[lane & 1], w = d4[(lane & 1) ^ 1];
+                    mn = fminf(fminf(fminf(u.x, u.y), fminf(u.z, u.w)), fminf(fminf(w.x, w.y), fminf(w.z, w.w)));
+                    mx = fmaxf(fmaxf(fmaxf(u.x, u.y), fmaxf(u.z, u.w)), fmaxf(fmaxf(w.x, w.y), fmaxf(w.z, w.w)));
+                } else {
+                    int jj = crot;  // rotated start: conflict-free banks across lanes
+                    for (int j = 0; j < clen; ++j) {
+                        const float x = sm.depth[sh4 + cst + jj];
+                        jj = jj + 1 == clen ? 0 : jj + 1;
+                        mn = fminf(mn, x);
+                        mx = fmaxf(mx, x);
+                    }
                 }
                 atomicMin(&sm.nearu[cq], f2ord(mn));
                 atomicMax(&sm.faru[cq], f2ord(mx));

@@ -446,7 +446,7 @@ WOIT_D WSmem<R, GEN> wcarve(unsigned char* base, const WLayout& L) {
 // step-wise accumulate / from-buffer branches compile out; GEN && !FUS serves the
 // step1..step4 entry points.
 template <int R, bool GEN, bool FUS>
-__global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel(const KParams kp) {
+__global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel(const __grid_constant__ KParams kp) {
     using G = WT<R>;
     constexpr int S = G::S, V = G::V, CH = G::CH, WC = 32, FBW = G::FBW, WIN = G::WIN, SUBP = G::SUBP;
     constexpr int VR = G::VR;  // padded row of the cell table: (pixel, channel) lanes hit distinct banks
@@ -1141,7 +1141,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
 constexpr int kLongT = 256;
 
 template <int R>
-__global__ void __launch_bounds__(kLongT) long_pixel_kernel(const KParams kp) {
+__global__ void __launch_bounds__(kLongT) long_pixel_kernel(const __grid_constant__ KParams kp) {
     constexpr int S = 1 << (R + 1), V = 3 * S, M = S;
     constexpr int TL = R <= 3 ? kLongT : (kLongT >> (R - 3));  // keep acc64 <= 96 KB
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1405,7 +1405,7 @@ cudaError_t launch_frame(const KParams& kp, cudaStream_t st) {
 
 // step4 alone: per-pixel composite from the buffers
 template <int R>
-__global__ void composite_kernel(const KParams kp) {
+__global__ void composite_kernel(const __grid_constant__ KParams kp) {
     constexpr int S = 1 << (R + 1), V = 3 * S;
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= kp.f.npix) return;

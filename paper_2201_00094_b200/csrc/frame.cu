@@ -210,7 +210,8 @@ WOIT_D void build_accum(float* __restrict__ part, float* __restrict__ sink, int 
 // The chunk loops visit fragment (crot + j) mod clen at step j. (Fully unrolled
 // loops for full chunks measured 3.5% slower: code size. Software pipelining of
 // this loop -- the next fragment's prep beside this one's updates, WOIT_BPIPE --
-// measured 4% slower; the evaluation loop's pipelining pays.)
+// measured 4% slower, and so did two fragments per step with paired fp32 ops
+// across them (3%); the evaluation loop's pipelining pays.)
 template <int R>
 WOIT_D void build_chunk_fast(zfix_t* WOIT_ZR zf, const float* WOIT_ZR dep, const DepthMap m,
                              const float* __restrict__ alp, float* __restrict__ trs, float* __restrict__ part,

@@ -9,9 +9,11 @@ the fused kernel: bounds, closed-form Haar build, per-fragment transmittance v̂
 (written, 12 B/fragment), visibility-weighted accumulation and composite (image
 written). Inputs (2.1 GB) are larger than L2 (126 MB), so no flush is needed.
 
-Multi-GPU (torchrun, one rank per GPU): weak scaling, rank r renders rows
-[1080 r, 1080 (r+1)) of a 1920 x 1080N frame and the fp32 image bands are
-all-gathered over NCCL inside the timed step; time = max over ranks.
+Multi-GPU (torchrun, one rank per GPU): config 2 scales weakly -- rank r renders
+rows [1080 r, 1080 (r+1)) of a 1920 x 1080N frame; --config 4 (BASELINE configs[3],
+4K x 128 particles) scales strongly -- the one 4K frame is split into N equal row
+bands. Either way the fp32 image bands are all-gathered over NCCL inside the timed
+step, and time = max over ranks.
 
 --impl reference times the reference's CPU algorithm (the numpy port in oracle/,
 a float64 restatement pinned against the reference's own outputs) on the host
@@ -40,8 +42,8 @@ REF_BUDGET_S = 150.0  # --impl reference: wall-clock budget for all W + K steps
 CONFIGS = {
     2: dict(workload="smoke", width=1920, height=1080, layers=32, rank=3, seed=1,
             name="config2: 1080p synthetic smoke, 32 frag/px, rank 3 (16 coeffs), 1 B200"),
-    4: dict(workload="particles", width=3840, height=2160, layers=128, rank=3, seed=1,
-            name="config4: 4K particles, 128 frag/px, depth-varying alpha, rank 3"),
+    4: dict(workload="particles", width=3840, height=2160, layers=128, rank=3, seed=1, strong=True,
+            name="config4: 4K particles, 128 frag/px, depth-varying alpha, rank 3, row bands over the GPUs"),
 }
 
 
@@ -185,10 +187,18 @@ def run_ours(args, cfg):
 
         dist.init_process_group("nccl", device_id=dev)
         pg = dist
-    H1 = cfg["height"]
     Wd = cfg["width"]
-    frame_h = H1 * world
-    # this rank's band of a weak-scaled frame: rows [H1*rank, H1*(rank+1))
+    strong = bool(cfg.get("strong"))
+    if strong:
+        # config 4: one frame, screen-sharded into equal row bands (strong scaling)
+        frame_h = cfg["height"]
+        if frame_h % world:
+            raise SystemExit(f"--config 4 needs the GPU count to divide {frame_h} rows")
+        H1 = frame_h // world
+    else:
+        # config 2: every GPU renders a 1080-row band of a 1920 x 1080N frame (weak scaling)
+        H1 = cfg["height"]
+        frame_h = H1 * world
     frame = W.FrameFragments.synthetic(cfg["workload"], Wd, frame_h, seed=cfg["seed"], layers=cfg["layers"],
                                        row0=H1 * rank, rows=H1, device=dev)
     rcfg = W.RenderConfig(rank=cfg["rank"], width=Wd, height=frame_h)
@@ -246,7 +256,11 @@ def run_ours(args, cfg):
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         total_ms, kern_ms = float(t[0]), float(t[1])
     ms = total_ms / args.steps
-    frags_total = n * world
+    frags_total = n
+    if world > 1:
+        tn = torch.tensor([n], dtype=torch.int64, device=dev)
+        pg.all_reduce(tn)
+        frags_total = int(tn.item())
     value = frags_total / (ms * 1e-3) / 1e9
 
     # end to end through the public API: pinned host stream -> device, render, image -> host
@@ -276,7 +290,8 @@ def run_ours(args, cfg):
                "sample": f"{sample}, 1 warm-up + {CPU_STEPS} timed renders ({CPU_STEPS * secs:.1f} s)"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if strong else "weak",
         "vs_baseline": None, "dtype": "f32 (z, indices and per-pixel sums in f64)", "data": "synthetic",
         "config": {"workload": cfg["name"], "width": Wd, "height": frame_h, "frag_per_px": cfg["layers"],
                    "rank": cfg["rank"], "fragments": frags_total, "l2_flush": f"inputs {frame_in_bytes / 1e9:.1f} GB/GPU > 126 MB L2",

@@ -43,7 +43,7 @@ int check_frags(const woit_frags_t* f, bool need_frag_arrays) {
 void fill_taps(KParams& kp) {
     const int k = kp.p.aberration_taps;
     kp.taps.n = 0;
-    kp.taps.pad = 0;
+    kp.taps.unit = 0;
     if (!(kp.p.flags & WOIT_CHROMATIC_ABERRATION) || k < 3 || k > kMaxTapTable) return;
     const bool lit = kp.p.flags & WOIT_LITERAL_SPECTRAL_T;
     for (int i = 0; i < k; ++i) {
@@ -52,6 +52,10 @@ void fill_taps(KParams& kp) {
         kp.taps.fac[i] = two_i / (double)(k - 1);
     }
     kp.taps.n = k;
+    int unit = 1;
+    for (int i = 0; i < k; ++i)
+        for (int c = 0; c < 3; ++c) unit &= (kp.taps.w[i][c] == 0.0 || kp.taps.w[i][c] == 1.0) ? 1 : 0;
+    kp.taps.unit = unit;
 }
 
 int run_frame(const woit_frags_t* f, const woit_params_t* p, woit_bufs_t* b, uint32_t phases, void* ws,

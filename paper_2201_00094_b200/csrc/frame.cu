@@ -4,7 +4,7 @@
 // Work decomposition:
 //   CTA      = a window of PB consecutive pixels of the band, split into
 //              sub-tiles of <= FB fragments / <= T chunks;
-//   chunk    = <= 16 consecutive fragments of ONE pixel, owned by one thread;
+//   chunk    = <= 8 consecutive fragments of ONE pixel, owned by one lane;
 //   staging  = the sub-tile's fragment fields copied global->shared by TMA
 //              bulk copies (cp.async.bulk + mbarrier), read once from HBM;
 //   per-pixel reductions (bounds, coefficients, accumulators) combine the
@@ -37,6 +37,12 @@
 #ifndef WOIT_BPIPE
 #define WOIT_BPIPE 0
 #endif
+#ifndef WOIT_MINB  // launch bound: minimum resident 1-warp CTAs per SM (14: <= 144 registers; ptxas then picks 127, measured best)
+#define WOIT_MINB 14
+#endif
+#ifndef WOIT_DEEPCOMB  // deep-pixel combine: lanes split over cell blocks
+#define WOIT_DEEPCOMB 1
+#endif
 #ifndef WOIT_FFMA2
 #define WOIT_FFMA2 1
 #endif
@@ -49,16 +55,6 @@ constexpr int kZUnroll = WOIT_ZUNROLL;  // z-loop unroll
 }
 
 namespace woit {
-
-// chunk descriptor: pixel (8 bits), start within sub-tile (13 bits), length (5 bits)
-WOIT_D uint32_t pack_chunk(int q, int start, int len) {
-    return (uint32_t)q | ((uint32_t)start << 8) | ((uint32_t)len << 21);
-}
-WOIT_D void unpack_chunk(uint32_t c, int& q, int& start, int& len) {
-    q = (int)(c & 255u);
-    start = (int)((c >> 8) & 8191u);
-    len = (int)(c >> 21);
-}
 
 // Within-chunk iteration starts at a rotation that depends only on the global
 // fragment id of the chunk start: it spreads the lanes of a warp over the 32
@@ -132,6 +128,35 @@ WOIT_D void haar_cells(const double c[], double cell[]) {
     }
     (void)width;
     (void)S;
+}
+
+// Sum over a pixel's nc chunk partials of one cell (pvk = the cell's row at the
+// pixel's first chunk). The order is a function of the cell's rotation km = k mod ng
+// and nc only: whole 4-chunk groups (nc % 4 == 0) are visited from group km on,
+// each group in chunk order; otherwise all chunks in order. With one group this is
+// plain chunk order. Rotating by the cell spreads the lanes of the deep-pixel
+// combine (one lane per cell block) over the shared-memory banks.
+template <int WC>
+WOIT_D float cell_sum(const float* pvk, int nc, int km, bool al4) {
+    float r = 0.0f;
+    if ((nc & 3) == 0) {
+        const int ng = nc >> 2;
+        int g = km;
+#pragma unroll 1
+        for (int s = 0; s < ng; ++s) {
+            const float* pg = pvk + 4 * g;
+            const float4 p4 = al4 ? *reinterpret_cast<const float4*>(pg) : make_float4(pg[0], pg[1], pg[2], pg[3]);
+            r += p4.x;
+            r += p4.y;
+            r += p4.z;
+            r += p4.w;
+            g = g + 1 == ng ? 0 : g + 1;
+        }
+    } else {
+#pragma unroll 1
+        for (int i = 0; i < nc; ++i) r += pvk[i];
+    }
+    return r;
 }
 
 // cell table entry (v_c, v_{c+1} - v_c) for one (pixel, channel) of the sub-tile;
@@ -361,7 +386,20 @@ WOIT_D void empty_run(const KParams& kp, int64_t p0, int ne, int lane) {
     if (kp.b.coeffs) {
         float* c = kp.b.coeffs + p0 * V;
         const bool packed = GEN && (flags & WOIT_PACKED_STORAGE);
-        for (int i = lane; i < ne * V; i += 32) c[i] = (packed && (i % V) >= 3) ? -0.0f : 0.0f;
+        if (V % 4 == 0 && (reinterpret_cast<uintptr_t>(c) & 15u) == 0) {
+            constexpr int V4 = V / 4 > 0 ? V / 4 : 1;
+            float4* c4 = reinterpret_cast<float4*>(c);
+            for (int i = lane; i < ne * V4; i += 32) {
+                float4 z = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                if (packed) {
+                    const float l0 = (i % V4) == 0 ? 0.0f : -0.0f;
+                    z = make_float4(l0, l0, l0, -0.0f);
+                }
+                c4[i] = z;
+            }
+        } else {
+            for (int i = lane; i < ne * V; i += 32) c[i] = (packed && (i % V) >= 3) ? -0.0f : 0.0f;
+        }
     }
     if (lane >= ne) return;
     const int64_t p = p0 + lane;
@@ -395,7 +433,6 @@ struct WSmem {
     double* den;
     double* rcp;
     double* vtot;      // [WIN][3] exp(-A_total)
-    uint32_t* chunk;   // [32]   chunk descriptors
     float* depth;      // staging [FBW+4] (granule-aligned window)
     float* alpha;
     float* trans;      // [FBW+4][3]
@@ -404,6 +441,9 @@ struct WSmem {
     float* normal;
     uint8_t* bf;
     zfix_t* zfix;      // [FBW] z in fixed point, by fragment
+#if !WOIT_CHUNKLANE
+    uint32_t* chunk;   // [32]
+#endif
     float* part;       // [V][32] chunk partials (f64 [WIN][V] scratch for packed storage)
     float2* cells;     // [SUBP][M][3] (v_c, v_{c+1} - v_c): staircase at cell centres
     float* coef32;     // [WIN][V] coefficients, bulk-stored to bufs->coeffs
@@ -424,7 +464,6 @@ WOIT_D WSmem<R, GEN> wcarve(unsigned char* base, const WLayout& L) {
     s.den = reinterpret_cast<double*>(base + L.den);
     s.rcp = reinterpret_cast<double*>(base + L.rcp);
     s.vtot = reinterpret_cast<double*>(base + L.vtot);
-    s.chunk = reinterpret_cast<uint32_t*>(base + L.chunk);
     s.depth = reinterpret_cast<float*>(base + L.depth);
     s.alpha = reinterpret_cast<float*>(base + L.alpha);
     s.trans = reinterpret_cast<float*>(base + L.trans);
@@ -433,6 +472,9 @@ WOIT_D WSmem<R, GEN> wcarve(unsigned char* base, const WLayout& L) {
     s.normal = reinterpret_cast<float*>(base + L.normal);
     s.bf = reinterpret_cast<uint8_t*>(base + L.bf);
     s.zfix = reinterpret_cast<zfix_t*>(base + L.zfix);
+#if !WOIT_CHUNKLANE
+    s.chunk = reinterpret_cast<uint32_t*>(base + L.chunk);
+#endif
     s.part = reinterpret_cast<float*>(base + L.part);
     s.cells = reinterpret_cast<float2*>(base + L.cells);
     s.coef32 = reinterpret_cast<float*>(base + L.coef32);
@@ -447,7 +489,7 @@ WOIT_D WSmem<R, GEN> wcarve(unsigned char* base, const WLayout& L) {
 // step-wise accumulate / from-buffer branches compile out; GEN && !FUS serves the
 // step1..step4 entry points.
 template <int R, bool GEN, bool FUS>
-__global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel(const __grid_constant__ KParams kp) {
+__global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R>::WPB) frame_kernel(const __grid_constant__ KParams kp) {
     using G = WT<R>;
     constexpr int S = G::S, V = G::V, CH = G::CH, WC = 32, FBW = G::FBW, WIN = G::WIN, SUBP = G::SUBP;
     constexpr int VR = G::VR;  // padded row of the cell table: (pixel, channel) lanes hit distinct banks
@@ -704,20 +746,50 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
             __syncwarp();
         }
 
-        // ---- 2. chunk table + per-pixel init (overlaps the copies) -----------------
+        // ---- 2. chunks + per-pixel init (overlaps the copies) -----------------------
+        // lane l < C owns chunk l of the sub-tile: its pixel q is the number of sub-tile
+        // pixels whose chunks end at or before l, and chunk i of a pixel is fragments
+        // [CH i, min(CH (i+1), run)) -- a function of the run length only, so the
+        // reduction order never depends on the tiling
+#if WOIT_CHUNKLANE
+        int cq = 0, cst = 0, clen = 0, crot = 0;
+        if (lane < C) {
+            const int cb0 = sm.cb[q0];
+#pragma unroll
+            for (int j = 1; j < SUBP; ++j) cq += (j < nqs && sm.cb[q0 + j] - cb0 <= lane) ? 1 : 0;
+            const int q = q0 + cq;
+            const int st = (lane - (sm.cb[q] - cb0)) * CH;
+            const int64_t oq = sm.offs[q];
+            const int run = (int)(sm.offs[q + 1] - oq);
+            cst = (int)(oq - fa) + st;
+            clen = run - st < CH ? run - st : CH;
+            crot = chunk_rotation(kp.f.frag_base + fa + cst, clen);
+        }
+#else
+        int cq = 0, cst = 0, clen = 0, crot = 0;
         if (lane < nqs) {
             const int q = q0 + lane;
             const int run = (int)(sm.offs[q + 1] - sm.offs[q]);
             const int nc = (sm.cb[q + 1] - sm.cb[q]);
             const int base = sm.cb[q] - sm.cb[q0];
             const int rel = (int)(sm.offs[q] - fa);
-            // chunk i of the pixel = fragments [CH i, min(CH (i+1), run)): a function of
-            // the run length only, so the reduction order never depends on the tiling
             for (int i = 0; i < nc; ++i) {
                 const int st = i * CH;
-                sm.chunk[base + i] = pack_chunk(lane, rel + st, run - st < CH ? run - st : CH);
+                sm.chunk[base + i] = (uint32_t)lane | ((uint32_t)(rel + st) << 8) |
+                                     ((uint32_t)(run - st < CH ? run - st : CH) << 21);
             }
-            const int64_t p = w0 + q;
+        }
+        __syncwarp();
+        if (lane < C) {
+            const uint32_t cd = sm.chunk[lane];
+            cq = (int)(cd & 255u);
+            cst = (int)((cd >> 8) & 8191u);
+            clen = (int)(cd >> 21);
+            crot = chunk_rotation(kp.f.frag_base + fa + cst, clen);
+        }
+#endif
+        if (lane < nqs) {
+            const int64_t p = w0 + q0 + lane;
             const bool init_empty = (ph & PH_BOUNDS) && !(ph & PH_BOUNDS_ACC);
             sm.nearu[lane] = f2ord(init_empty ? INFINITY : kp.b.near[p]);
             sm.faru[lane] = f2ord(init_empty ? -INFINITY : kp.b.far[p]);
@@ -727,13 +799,6 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
             parity ^= 1u;
         }
         __syncwarp();
-
-        // this lane's chunk (lanes >= C idle in the fragment phases)
-        int cq = 0, cst = 0, clen = 0, crot = 0;
-        if (lane < C) {
-            unpack_chunk(sm.chunk[lane], cq, cst, clen);
-            crot = chunk_rotation(kp.f.frag_base + fa + cst, clen);
-        }
 
         // ---- 3. bounds (step1) ------------------------------------------------------
         if (ph & PH_BOUNDS) {
@@ -848,20 +913,118 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, 12 / WT<R>::WPB) frame_kernel
             // nqs <= SUBP keeps this to one round, so every lane has read its partials
             // before the region is reused for coefficients and cells.
             const int t = lane;
-            const bool task = t < nqs * 3;
+            const int ntask = nqs * 3;
+            const bool task = t < ntask;
             const int kch = task ? t / nqs : 0, kq = task ? t - kch * nqs : 0;
             double c[S];
             float rc[M];
-            if (task) {
+            // Few deep pixels (>= 64 fragments each, <= 4 per sub-tile): the (pixel,
+            // channel, cell block) sums are spread over the warp -- KB cells per lane, the
+            // cells k = blk + j B of a block, B = M / KB blocks per (pixel, channel) --
+            // and gathered through shared memory. Each cell's summation order is
+            // cell_sum's (a function of k and the run length only), so the split -- a
+            // function of the tiling -- never changes a bit of the result.
+            constexpr int B = M >= 8 ? 8 : M, KB = M / B, NR = (12 * B + 31) / 32;
+            if (WOIT_DEEPCOMB && nqs <= 4 && B > 1) {
+                constexpr int SR = M % 4 == 0 ? M + 4 : M + 1;  // [ntask][SR] scratch rows
+                float rs[NR][KB];
+                int nr = 0;
+#pragma unroll
+                for (int r = 0; r < NR; ++r) {  // ntask B <= 12 B lane tasks
+                    const int u = lane + 32 * r;
+                    const int tb = u / B, blk = u % B;
+                    if (tb < ntask) {
+                        ++nr;
+                        const int kchb = tb / nqs, kqb = tb - kchb * nqs;
+                        const int q = q0 + kqb;
+                        const int nc = (sm.cb[q + 1] - sm.cb[q]);
+                        const int cbq = sm.cb[q] - sm.cb[q0];
+                        const float* pv = part + kchb * WC + cbq;
+#pragma unroll
+                        for (int j = 0; j < KB; ++j) rs[r][j] = 0.0f;
+                        if ((nc & 3) == 0 && ((cbq & 3) == 0)) {
+                            const int ng = nc >> 2;
+                            int g[KB];
+#pragma unroll
+                            for (int j = 0; j < KB; ++j) g[j] = (blk + j * B) % ng;
+#pragma unroll 1
+                            for (int st = 0; st < ng; ++st) {
+#pragma unroll
+                                for (int j = 0; j < KB; ++j) {
+                                    const float4 p4 =
+                                        *reinterpret_cast<const float4*>(pv + (blk + j * B) * 3 * WC + 4 * g[j]);
+                                    rs[r][j] += p4.x;
+                                    rs[r][j] += p4.y;
+                                    rs[r][j] += p4.z;
+                                    rs[r][j] += p4.w;
+                                    g[j] = g[j] + 1 == ng ? 0 : g[j] + 1;
+                                }
+                            }
+                        } else {
+                            const int ng = (nc & 3) == 0 && nc > 0 ? nc >> 2 : 1;
+#pragma unroll
+                            for (int j = 0; j < KB; ++j)
+                                rs[r][j] = cell_sum<WC>(pv + (blk + j * B) * 3 * WC, nc, (blk + j * B) % ng, false);
+                        }
+                    }
+                }
+                __syncwarp();  // every lane has read its partials: the region takes the sums
+#pragma unroll
+                for (int r = 0; r < NR; ++r) {
+                    const int u = lane + 32 * r;
+                    if (r < nr) {
+#pragma unroll
+                        for (int j = 0; j < KB; ++j) part[(u / B) * SR + u % B + j * B] = rs[r][j];
+                    }
+                }
+                __syncwarp();
+                if (task) {
+                    if constexpr (M % 4 == 0) {
+#pragma unroll
+                        for (int k = 0; k < M; k += 4) {
+                            const float4 v4 = *reinterpret_cast<const float4*>(part + t * SR + k);
+                            rc[k] = v4.x;
+                            rc[k + 1] = v4.y;
+                            rc[k + 2] = v4.z;
+                            rc[k + 3] = v4.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < M; ++k) rc[k] = part[t * SR + k];
+                    }
+#pragma unroll
+                    for (int k = 1; k < M; ++k) rc[k] += rc[k - 1];
+                }
+            } else if (task) {
                 const int q = q0 + kq;
                 const int nc = (sm.cb[q + 1] - sm.cb[q]);
                 const int cbq = sm.cb[q] - sm.cb[q0];
                 const float* pv = part + kch * WC + cbq;
 #pragma unroll
                 for (int k = 0; k < M; ++k) rc[k] = 0.0f;
-                // chunks summed in chunk order (fixed by the pixel's run length only);
-                // 16-B vector loads when the pixel's chunk group is 4-aligned
-                if (((cbq | nc) & 3) == 0) {
+                if ((nc & 3) == 0 && nc > 4) {
+                    // whole 4-chunk groups, more than one: cell_sum's rotated group order
+                    // (cell k reads group (k + st) mod ng at step st), cells interleaved
+                    const int ng = nc >> 2;
+                    const bool al4 = (cbq & 3) == 0;
+#pragma unroll 1
+                    for (int st = 0; st < ng; ++st) {
+                        int g = st;
+#pragma unroll
+                        for (int k = 0; k < M; ++k) {
+                            const float* pg = pv + k * 3 * WC + 4 * g;
+                            const float4 p4 = al4 ? *reinterpret_cast<const float4*>(pg)
+                                                  : make_float4(pg[0], pg[1], pg[2], pg[3]);
+                            rc[k] += p4.x;
+                            rc[k] += p4.y;
+                            rc[k] += p4.z;
+                            rc[k] += p4.w;
+                            g = g + 1 == ng ? 0 : g + 1;
+                        }
+                    }
+                } else if (((cbq | nc) & 3) == 0) {
+                    // one group (the common shallow case): cell_sum's order, all cells
+                    // interleaved for ILP, 16-B vector loads
 #pragma unroll 1
                     for (int i = 0; i < nc; i += 4) {
 #pragma unroll

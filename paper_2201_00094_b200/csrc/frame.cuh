@@ -32,7 +32,7 @@ enum : uint32_t {
 constexpr int kMaxTapTable = 65;
 struct TapTable {
     int32_t n;  // taps tabulated; 0 (k > kMaxTapTable): computed in the kernel
-    int32_t pad;
+    int32_t unit;  // every weight exactly 0 or 1: a zero-offset gather is the pixel itself
     double fac[kMaxTapTable];   // 2 i / (k - 1)
     double w[kMaxTapTable][3];  // spectral_weight(i, k)
 };
@@ -61,6 +61,10 @@ struct WT {
     static constexpr int WPB = R <= 3 ? WOIT_WPB : 1;  // warps per CTA
     static constexpr int VR = V + ((35 - V % 32) % 32);  // row stride == 3 (mod 32), >= V
 };
+
+#ifndef WOIT_CHUNKLANE  // chunk descriptors computed by each chunk lane (no table)
+#define WOIT_CHUNKLANE 1
+#endif
 
 struct WLayout {
     uint32_t offs, cb, nearu, faru, lo, den, rcp, vtot, chunk;
@@ -96,7 +100,7 @@ WOIT_HD WLayout make_wlayout(uint32_t phases, int flags, bool alias_z) {
     L.rcp = o;   o = align16(o + 8u * G::SUBP);
     L.vtot = o;  o = align16(o + 8u * 3 * G::SUBP);
     static_assert(8 * 6 * G::SUBP >= 4 * 3 * 32, "sink overlay too small");
-    L.chunk = o; o = align16(o + 4u * 32);
+    L.chunk = o; o = align16(o + (WOIT_CHUNKLANE ? 0u : 4u * 32));
     L.depth = o; o = align16(o + 4u * FS);
     L.alpha = o; o = align16(o + (at ? 4u * FS : 0u));
     L.trans = o; o = align16(o + (at ? 12u * FS : 0u));
@@ -225,7 +229,9 @@ WOIT_D double sample_background_ch(const float* img, int W, int H, int64_t gp, i
             // every tap lands on the pixel itself, where the bilinear weights are exactly
             // (1, 0) and the sample is exactly the pixel: same arithmetic, no gathers
             const double s0 = (double)img[gp * 3 + ch];
-            if (!(flags & WOIT_CHROMATIC_ABERRATION)) return s0;
+            // with 0/1 weights (k = 3, 5, 7) the sum is m s0 exactly (s0 is fp32-valued)
+            // and m s0 / m == s0: the pixel itself, bit for bit
+            if (!(flags & WOIT_CHROMATIC_ABERRATION) || (tt.n == taps && tt.unit)) return s0;
             const bool lit = flags & WOIT_LITERAL_SPECTRAL_T;
             double num = 0.0, den = 0.0;
             for (int i = 0; i < taps; ++i) {
@@ -261,6 +267,12 @@ WOIT_D void sample_background(const float* img, int W, int H, int64_t gp, int fl
                               const TapTable& tt, double ox, double oy, double bg[3]) {
     if (flags & (WOIT_CHROMATIC_ABERRATION | WOIT_REFRACTION)) {
         const double px = (double)(gp % W), py = (double)(gp / W);
+        if (ox == 0.0 && oy == 0.0 && (!(flags & WOIT_CHROMATIC_ABERRATION) || (tt.n == taps && tt.unit))) {
+            // exact bilinear weights (1, 0) at the pixel, 0/1 tap weights: the pixel itself
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) bg[ch] = (double)img[gp * 3 + ch];
+            return;
+        }
         if (flags & WOIT_CHROMATIC_ABERRATION) {
             const bool lit = flags & WOIT_LITERAL_SPECTRAL_T;
             double num[3] = {0.0, 0.0, 0.0}, den[3] = {0.0, 0.0, 0.0};

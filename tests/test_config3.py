@@ -1,8 +1,8 @@
 """Config 3 at full size: the reference's wine-bottle frame at
 1920x1080 with refraction + aberration (k=5) + cubed transmission, GPU vs the
 float64 oracle on the same fp32 inputs. The input (the reference's cast_frame
-output) is written by tools/make_config3.py into data/ (git-ignored); the test
-skips when it is absent."""
+output) is written by tools/make_config3.py into data/ (git-ignored); without it the
+frame comes from the on-device caster (CSR pinned to the reference's by tests/test_cast.py)."""
 
 import os
 
@@ -13,7 +13,7 @@ import torch
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 DATA = os.path.join(REPO, "data", "config3_wine_1080p.npz")
 
-pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not os.path.exists(DATA), reason="data/ config-3 stream absent")]
+pytestmark = pytest.mark.gpu
 
 
 def test_config3_full_frame_matches_oracle():

@@ -209,6 +209,28 @@ def test_band_split_is_bit_identical(W):
     assert torch.equal(a, b) and torch.equal(a, c)
 
 
+@pytest.mark.parametrize("layers", [128, 256])
+def test_deep_band_split_is_bit_identical(W, layers):
+    """Deep ragged pixels: sub-tiles of one to a few pixels, so the deep-pixel combine's
+    lane split changes with the band split; the images, coefficients and v̂ must not,
+    and they match the oracle."""
+    sf = W.synth.generate("ragged", 37, 23, seed=13, layers=layers)
+    frame = W.FrameFragments.from_synth(sf)
+    outs = [W.render_frame(None, W.RenderConfig(rank=3, width=37, height=23, workers=k), frame=frame)
+            for k in (1, 3, 7)]
+    assert all(torch.equal(outs[0], o) for o in outs[1:])
+    cfg = W.RenderConfig(rank=3, width=37, height=23)
+    full = W.render_band(frame, cfg, vhat=True)
+    bands = [W.render_band(frame.band(p0, p1), cfg, vhat=True) for p0, p1 in ((0, 37 * 5), (37 * 5, 37 * 23))]
+    torch.cuda.synchronize()
+    for name in ("coeffs", "vhat"):
+        assert torch.equal(getattr(full, name), torch.cat([getattr(b, name) for b in bands])), name
+    ref = O.render_frame(O.OFrame.from_synth(sf), O.OConfig(rank=3, width=37, height=23))
+    assert np.abs(h(full.coeffs) - ref.coeffs).max() <= 1e-5
+    assert np.abs(h(full.vhat) - ref.vhat).max() <= 1e-5
+    assert np.abs(h(full.output) - ref.output).max() <= 1e-4
+
+
 def test_repeat_runs_bit_identical(W):
     frame = W.FrameFragments.synthetic("particles", 64, 32, seed=4, layers=128)
     cfg = W.RenderConfig(rank=3, width=64, height=32)

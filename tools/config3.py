@@ -30,12 +30,22 @@ DATA = os.path.join(REPO, "data", "config3_wine_1080p.npz")
 
 
 def load():
-    d = np.load(DATA)
-    Wd, H = int(d["width"]), int(d["height"])
-    sf = synth.SynthFrame(Wd, H, 0, H, d["offsets"], d["depth"], d["alpha"], d["trans"], d["radiance"],
-                          d["normal"], d["ior"], d["backface"], d["opaque_depth"], d["opaque_color"])
-    cam = dict(position=tuple(d["cam_position"]), forward=tuple(d["cam_forward"]), fov_deg=float(d["cam_fov"]))
-    return sf, cam
+    """The config-3 stream: data/config3_wine_1080p.npz (the reference's own cast_frame
+    output) when present, else the on-device caster's cast of the same preset (its CSR is
+    identical to the reference's and its values within one fp32 rounding, tests/test_cast.py)."""
+    if os.path.exists(DATA):
+        d = np.load(DATA)
+        Wd, H = int(d["width"]), int(d["height"])
+        sf = synth.SynthFrame(Wd, H, 0, H, d["offsets"], d["depth"], d["alpha"], d["trans"], d["radiance"],
+                              d["normal"], d["ior"], d["backface"], d["opaque_depth"], d["opaque_color"])
+        cam = dict(position=tuple(d["cam_position"]), forward=tuple(d["cam_forward"]), fov_deg=float(d["cam_fov"]))
+        return sf, cam
+    from paper_2201_00094_b200 import scene as S
+
+    sc = S.preset("wine-bottle")
+    sf = S.cast_frame(sc, 1920, 1080).to_synth()
+    c = sc.camera
+    return sf, dict(position=tuple(c.position), forward=tuple(c.forward), fov_deg=float(c.fov_deg))
 
 
 CFG = dict(rank=3, refraction=True, chromatic_aberration=True, cube_transmission=True, aberration_taps=5)

@@ -44,6 +44,12 @@ CONFIGS = {
             name="config2: 1080p synthetic smoke, 32 frag/px, rank 3 (16 coeffs), 1 B200"),
     4: dict(workload="particles", width=3840, height=2160, layers=128, rank=3, seed=1, strong=True,
             name="config4: 4K particles, 128 frag/px, depth-varying alpha, rank 3, row bands over the GPUs"),
+    # config 5: the 8K x 256 stress frame is 8.5 G fragments (272 GB of fp32 stream), so
+    # it is the 8-GPU job: every GPU renders its 540-row eighth (1.06 G fragments);
+    # N GPUs render the first N eighths, N = 8 the whole frame. --rank 2/3/4 sweeps
+    # the coefficient count (8/16/32).
+    5: dict(workload="particles", width=7680, height=4320, layers=256, rank=3, seed=1, share=8,
+            name="config5: 8K stress, 256 frag/px, 540-row eighth of the frame per GPU"),
 }
 
 
@@ -189,7 +195,13 @@ def run_ours(args, cfg):
         pg = dist
     Wd = cfg["width"]
     strong = bool(cfg.get("strong"))
-    if strong:
+    if cfg.get("share"):
+        # config 5: the GPU's fixed share of the frame (weak scaling up to the full frame)
+        frame_h = cfg["height"]
+        if world > cfg["share"]:
+            raise SystemExit(f"--config {args.config} runs on at most {cfg['share']} GPUs")
+        H1 = frame_h // cfg["share"]
+    elif strong:
         # config 4: one frame, screen-sharded into equal row bands (strong scaling)
         frame_h = cfg["height"]
         if frame_h % world:
@@ -285,7 +297,9 @@ def run_ours(args, cfg):
         return
     cpu = None
     if world == 1 and not args.no_cpu:
-        v, cores, sample, secs = cpu_reference(cfg, args.ref_rows, CPU_STEPS, 1)
+        # a bounded sample: <= 14.7 M fragments (config 2: 240 rows)
+        rows = max(1, min(args.ref_rows, 14745600 // (cfg["width"] * cfg["layers"])))
+        v, cores, sample, secs = cpu_reference(cfg, rows, CPU_STEPS, 1)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"{sample}, 1 warm-up + {CPU_STEPS} timed renders ({CPU_STEPS * secs:.1f} s)"}
     line = {
@@ -298,7 +312,7 @@ def run_ours(args, cfg):
                    "parallelism": f"row bands x{world}, NCCL image all-gather" if world > 1 else "1 GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": args.traffic,
-                     "kernel": "frame_kernel<3> (fused bounds+build+eval+composite)",
+                     "kernel": f"frame_kernel<{cfg['rank']}> (fused bounds+build+eval+composite)",
                      "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": alg, "peak_kind": peak_kind},
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -365,6 +379,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", type=int, choices=sorted(CONFIGS), default=2)
+    ap.add_argument("--rank", type=int, default=None, help="override the config's rank (config 5 sweep)")
     ap.add_argument("--ref-rows", type=int, default=240, help="rows of the CPU sample")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -373,7 +388,12 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3  # timing rule: >= 3 warm-up steps
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.rank is not None:
+        if not 0 <= args.rank <= 6:
+            raise SystemExit("--rank must be in 0..6")
+        cfg["rank"] = args.rank
+        cfg["name"] += f" (rank {args.rank}: {2 << args.rank} coefficients)"
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -40,6 +40,9 @@
 #ifndef WOIT_MINB  // launch bound: minimum resident 1-warp CTAs per SM (14: <= 144 registers; ptxas then picks 127, measured best)
 #define WOIT_MINB 14
 #endif
+#ifndef WOIT_THIN  // thin sub-tiles (one pixel per lane) for shallow pixel runs
+#define WOIT_THIN 1
+#endif
 #ifndef WOIT_DEEPCOMB  // deep-pixel combine: lanes split over cell blocks
 #define WOIT_DEEPCOMB 1
 #endif
@@ -272,6 +275,53 @@ WOIT_D void build_chunk_fast(zfix_t* WOIT_ZR zf, const float* WOIT_ZR dep, const
 #endif
 }
 
+// Cell pair (v_c, v_{c+1} - v_c) for the evaluation. CellsPair reads the per-sub-tile
+// table store_cells wrote; CellsCol (thin sub-tiles) reads the lane's own staircase
+// column in the partials region and forms the difference the same way (fp32 v_{c+1} -
+// v_c; 0 for the last cell, where the evaluation's lerp weight is 0 anyway).
+struct CellsPair {
+    const float2* __restrict__ cq2;
+    WOIT_D float2 get(int c0, int ch) const { return cq2[c0 * 3 + ch]; }
+};
+template <int M>
+struct CellsCol {
+    const float* __restrict__ col;  // part + lane: row stride 3 x 32 floats per cell
+    WOIT_D float2 get(int c0, int ch) const {
+        const float v0 = col[c0 * 96 + ch * 32];
+        const int c1 = c0 + 1 < M ? c0 + 1 : c0;
+        return make_float2(v0, col[c1 * 96 + ch * 32] - v0);
+    }
+};
+
+// Haar analysis of the staircase (cell averages T[0..M)) in f64, wavelet.py:3-9
+// layout: c[2^n + k] = 2^(n/2)/M (sum left half - sum right half), c[0] = mean.
+// T is consumed.
+template <int R>
+WOIT_D void haar_analysis(double T[], double c[]) {
+    constexpr int M = 2 << R;
+#pragma unroll
+    for (int m = 0; m <= R; ++m) {
+        const int half = M >> (m + 1);  // wavelets at level n = R - m
+#pragma unroll
+        for (int k = 0; k < half; ++k) {
+            const double x = T[2 * k], y = T[2 * k + 1];
+            c[half + k] = dmul(dmul(dsub(x, y), kSqrt2Pow[R - m]), 1.0 / M);
+            T[k] = dadd(x, y);
+        }
+    }
+    c[0] = dmul(T[0], 1.0 / M);
+}
+
+// Composite of one channel on the fast path (no refraction / aberration: the
+// background is the pixel's opaque colour), pipeline.py:284-308.
+WOIT_D float composite_fast_ch(int flags, double acc, double wgt, double bg, double vt) {
+    if (flags & WOIT_NORMALIZE) {
+        const double avg = acc * rcp_refined(fmax(kNormEps, wgt));
+        return (float)dadd(dmul(avg, 1.0 - vt), dmul(bg, vt));
+    }
+    return (float)dadd(acc, dmul(bg, vt));
+}
+
 template <int R>
 WOIT_D void eval_frag(const zfix_t* __restrict__ zf, const float* __restrict__ alp, const float* __restrict__ opw,
                       const float2* __restrict__ cq2, float* __restrict__ rad, int fr, int si, float ac[3],
@@ -292,9 +342,9 @@ WOIT_D void eval_frag(const zfix_t* __restrict__ zf, const float* __restrict__ a
     }
 }
 
-template <int R>
+template <int R, typename CELLS>
 WOIT_D void eval_chunk_fast(const zfix_t* __restrict__ zf, const float* __restrict__ alp,
-                            const float* __restrict__ opw, const float2* __restrict__ cq2,
+                            const float* __restrict__ opw, const CELLS cq2,
                             float* __restrict__ rad, int cst, int clen, int crot, int sh4, float ac[3],
                             float wg[3]) {
 #if WOIT_EVPIPE
@@ -315,7 +365,7 @@ WOIT_D void eval_chunk_fast(const zfix_t* __restrict__ zf, const float* __restri
         for (int ch = 0; ch < 3; ++ch) {
             L[ch] = rad[3 * (sh4 + fr) + ch];
             op[ch] = opw[3 * (sh4 + fr) + ch];
-            vd[ch] = cq2[c0 * 3 + ch];
+            vd[ch] = cq2.get(c0, ch);
         }
     }
 #pragma unroll 1
@@ -332,7 +382,7 @@ WOIT_D void eval_chunk_fast(const zfix_t* __restrict__ zf, const float* __restri
         for (int ch = 0; ch < 3; ++ch) {
             Ln[ch] = rad[3 * sin + ch];
             opn[ch] = opw[3 * sin + ch];
-            vdn[ch] = cq2[cn * 3 + ch];
+            vdn[ch] = cq2.get(cn, ch);
         }
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
@@ -359,7 +409,7 @@ WOIT_D void eval_chunk_fast(const zfix_t* __restrict__ zf, const float* __restri
     for (int j = 0; j < clen; ++j) {
         const int fr = cst + jj;
         jj = jj + 1 == clen ? 0 : jj + 1;
-        eval_frag<R>(zf, alp, opw, cq2, rad, fr, sh4 + fr, ac, wg);
+        eval_frag<R>(zf, alp, opw, cq2.cq2, rad, fr, sh4 + fr, ac, wg);
     }
 #endif
 }
@@ -488,7 +538,7 @@ WOIT_D WSmem<R, GEN> wcarve(unsigned char* base, const WLayout& L) {
 // FUS: the phases are the fused render's (compile-time constant), so the
 // step-wise accumulate / from-buffer branches compile out; GEN && !FUS serves the
 // step1..step4 entry points.
-template <int R, bool GEN, bool FUS>
+template <int R, bool GEN, bool FUS, bool THIN>
 __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R>::WPB) frame_kernel(const __grid_constant__ KParams kp) {
     using G = WT<R>;
     constexpr int S = G::S, V = G::V, CH = G::CH, WC = 32, FBW = G::FBW, WIN = G::WIN, SUBP = G::SUBP;
@@ -530,6 +580,9 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
     const bool need_ior = do_at && (cube || refr);
     const bool packed = GEN && (flags & WOIT_PACKED_STORAGE);
     const int64_t nalloc = kp.f.nfrag;
+    // thin sub-tiles: the fused render without packed storage, when the coefficient
+    // transpose ([V][33] floats) fits over the depth / alpha / T / L staging arrays
+    const bool kThinOK = THIN && FUS && !packed && V * 33 * 4 <= (int)(L.rad - L.depth) + 12 * (FBW + 4);
 
     if (lane == 0) mbar_init(sm.bar, 1);
     uint32_t parity = 0;
@@ -560,18 +613,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
         }
         if (kp.b.accum) kp.b.accum[p * 3 + kch] = (float)acc;
         if (kp.b.weight) kp.b.weight[p * 3 + kch] = (float)wgt;
-        if (kp.b.output) {
-            const double bg = (double)bgr;
-            const double vt = sm.vtot[kq * 3 + kch];
-            double o;
-            if (flags & WOIT_NORMALIZE) {
-                const double avg = acc * rcp_refined(fmax(kNormEps, wgt));
-                o = dadd(dmul(avg, 1.0 - vt), dmul(bg, vt));
-            } else {
-                o = dadd(acc, dmul(bg, vt));
-            }
-            kp.b.output[p * 3 + kch] = (float)o;
-        }
+        if (kp.b.output) kp.b.output[p * 3 + kch] = composite_fast_ch(flags, acc, wgt, (double)bgr, sm.vtot[kq * 3 + kch]);
         if (kch == 0 && kp.b.refraction_offset) {
             kp.b.refraction_offset[p * 2] = 0.0f;
             kp.b.refraction_offset[p * 2 + 1] = 0.0f;
@@ -589,6 +631,55 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
             composite_fast(pq0, pnqs, pw0, pending_bg());
             pend = false;
             __syncwarp();
+        }
+    };
+    int64_t eg_fa = 0;  // the current sub-tile's first fragment (for eval_gen)
+    // general-path evaluation of one chunk (step 3, pipeline.py:170-217): v̂, the
+    // accumulators, the diffusion coverage and the refraction offsets; `cells` is the
+    // sub-tile's cell table (CellsPair) or the lane's staircase column (CellsCol)
+    auto eval_gen = [&](auto cells, int cst, int clen, int crot, const double d[3], double topq, float ac[3],
+                        float wg[3], float& df, double ro[2]) {
+        const int64_t fa_ = eg_fa;
+        const int sh4 = (int)(fa_ - (fa_ & ~(int64_t)3)), shb = (int)(fa_ - (fa_ & ~(int64_t)15));
+        const bool op_staged = ph & PH_BUILD;  // the build left alpha (1 - T') in the trans slot
+        int jj = crot;
+#pragma unroll kUnroll
+        for (int j = 0; j < clen; ++j) {
+            const int fr = cst + jj;
+            jj = jj + 1 == clen ? 0 : jj + 1;
+            const int si = sh4 + fr;
+            int c0;
+            float t;
+            eval_cell(sm.zfix[fr], R, c0, t);
+            const float al = sm.alpha[si];
+            bool cb_ = false;
+            float io = 1.0f;
+            if (need_ior) {
+                io = sm.ior[si];
+                cb_ = cube && io > 1.0f && (!bfonly || sm.bf[shb + fr] != 0);
+            }
+            float vs = 0.0f;
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+                // A = lerp of the two neighbouring cell centres, clamped >= 0 (wavelet.py:316-319)
+                const float2 vd = cells.get(c0, ch);
+                const float A = fmaxf(fmaf(t, vd.y, vd.x), 0.0f);
+                const float vh = exp_neg(A);
+                const float Lr = sm.rad[3 * si + ch];
+                const float op = op_staged ? sm.trans[3 * si + ch] : opacity_ch(al, sm.trans[3 * si + ch], cb_);
+                ac[ch] += (Lr * al) * vh;
+                wg[ch] += op * vh;
+                vs += vh;
+                sm.rad[3 * si + ch] = vh;  // v̂ replaces radiance in place
+            }
+            if (diffuse) df += al * vs;  // diffusion coverage (woit.h WOIT_DIFFUSION)
+            if (refr && io > 1.0f) {
+                const float nrm[3] = {sm.normal[3 * si], sm.normal[3 * si + 1], sm.normal[3 * si + 2]};
+                double off[2];
+                refraction_offset(kp, d, topq, sm.depth[si], nrm, io, off);
+                ro[0] += off[0];
+                ro[1] += off[1];
+            }
         }
     };
     int64_t next_win = nwin;
@@ -656,9 +747,23 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
             q0 += 1;
             continue;
         }
-        const int q1 = q0 + cnt;
+        // thin sub-tile: a run of > SUBP pixels from q0 with 1..CH fragments each (every
+        // pixel one chunk) is taken whole, one pixel per lane (shallow scenes)
+        bool thin = false;
+        int q1 = q0 + cnt;
+        if (kThinOK) {
+            const int q = q0 + lane;
+            const int64_t run = q < nq ? sm.offs[q + 1] - sm.offs[q] : 0;
+            const unsigned b = __ballot_sync(0xffffffffu, run >= 1 && run <= CH);
+            const int tc = b == 0xffffffffu ? 32 : __ffs(~b) - 1;
+            if (tc > SUBP) {
+                thin = true;
+                q1 = q0 + tc;
+            }
+        }
         const int nqs = q1 - q0;
         const int64_t fa = sm.offs[q0], fb = sm.offs[q1];
+        eg_fa = fa;
         const int C = sm.cb[q1] - sm.cb[q0];
         const int64_t a4 = fa & ~(int64_t)3, a16 = fa & ~(int64_t)15;
         const int sh4 = (int)(fa - a4);  // staging index of fragment fa (granule-4 arrays)
@@ -688,7 +793,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
             const int64_t pa = w0 + q0, pb = w0 + q1, pa4 = pa & ~(int64_t)3;
             int64_t pb4 = (pb + 3) & ~(int64_t)3;
             pb4 = pb4 < (kp.f.npix & ~(int64_t)3) ? pb4 : (kp.f.npix & ~(int64_t)3);
-            if (GEN || !kp.use_tma || pb4 < pa4) pb4 = pa4;
+            if (GEN || thin || !kp.use_tma || pb4 < pa4) pb4 = pa4;
             if (kp.use_tma && lane == 0) {
                 bulk_wait_read_all();  // the previous sub-tile's stores have left smem
                 const uint32_t n4 = (uint32_t)(b4 - a4);
@@ -725,7 +830,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
 #pragma unroll
                     for (int c = 0; c < 3; ++c) sm.normal[3 * si + c] = kp.f.normal[3 * i + c];
             }
-            if (!GEN)
+            if (!GEN && !thin)
                 for (int64_t p = (pb4 > pa ? pb4 : pa) + lane; p < pb; p += 32) {
                     const int si = (int)(p - pa4);
                     sm.opq[3 * si] = kp.f.opaque_color[3 * p];
@@ -744,6 +849,193 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
             composite_fast(pq0, pnqs, pw0, pbg);
             pend = false;
             __syncwarp();
+        }
+
+        if (kThinOK && thin) {
+            // ---- thin sub-tile: lane l owns pixel q0 + l, whose whole run is one chunk.
+            // Same operations, in the same order, as the general sub-tile with one
+            // chunk per pixel (bit-identical results), without the per-(pixel, channel)
+            // passes: the lane's column of the partials region holds D, then the
+            // staircase v in place, read back by its own evaluation.
+            const bool act = lane < nqs;
+            const int64_t p = w0 + q0 + lane;
+            int cst = 0, clen = 0, crot = 0;
+            if (act) {
+                const int64_t oq = sm.offs[q0 + lane];
+                clen = (int)(sm.offs[q0 + lane + 1] - oq);
+                cst = (int)(oq - fa);
+                crot = chunk_rotation(kp.f.frag_base + fa + cst, clen);
+            }
+            if (kp.use_tma) {
+                mbar_wait(sm.bar, parity);
+                parity ^= 1u;
+            }
+            __syncwarp();
+            // bounds (step 1)
+            float mn = INFINITY, mx = -INFINITY;
+            int jj = crot;
+            for (int j = 0; j < clen; ++j) {
+                const float x = sm.depth[sh4 + cst + jj];
+                jj = jj + 1 == clen ? 0 : jj + 1;
+                mn = fminf(mn, x);
+                mx = fmaxf(mx, x);
+            }
+            DepthMap m{0.0, 0.0, 0.0, 0.0};
+            if (act) {
+                if (kp.b.near) kp.b.near[p] = mn;
+                if (kp.b.far) kp.b.far[p] = mx;
+                m = depth_map(mn, mx, R);
+            }
+            // build (step 2) into the lane's column
+            float* part = sm.part;
+            {
+                float4* pz = reinterpret_cast<float4*>(part);
+                for (int i = lane; i < (M * 3 * WC) / 4; i += 32) pz[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            if (GEN && act) {
+                jj = crot;
+                for (int j = 0; j < clen; ++j) {
+                    const int fr = cst + jj;
+                    jj = jj + 1 == clen ? 0 : jj + 1;
+                    sm.zfix[fr] = z_fixed_of(sm.depth[sh4 + fr], m);
+                }
+            }
+            __syncwarp();
+            float* sink = reinterpret_cast<float*>(sm.lo) + lane;
+            if (act) {
+                if (!GEN) {
+                    build_chunk_fast<R>(sm.zfix + (WOIT_ALIASZ ? sh4 : 0), sm.depth, m, sm.alpha, sm.trans, part, sink,
+                                        lane, cst, clen, crot, sh4);
+                } else {
+                    jj = crot;
+                    for (int j = 0; j < clen; ++j) {
+                        const int fr = cst + jj;
+                        jj = jj + 1 == clen ? 0 : jj + 1;
+                        const int si = sh4 + fr;
+                        const zfix_t zi = sm.zfix[fr];
+                        const float al = sm.alpha[si];
+                        bool cb_ = false;
+                        if (cube) cb_ = sm.ior[si] > 1.0f && (!bfonly || sm.bf[shb + fr] != 0);
+                        float a[3];
+#pragma unroll
+                        for (int ch = 0; ch < 3; ++ch) {
+                            const float op = opacity_ch(al, sm.trans[3 * si + ch], cb_);
+                            sm.trans[3 * si + ch] = op;
+                            a[ch] = -log_poly(fmaxf((float)kTransFloor, 1.0f - op));
+                        }
+                        const int cell = (int)(zi >> (kZBits - (R + 1)));
+                        const float fr_ = u32_to_unit(zi << (R + 1), kZBits);
+                        float* dd = part + cell * 3 * WC + lane;
+                        float* d2 = cell + 1 < M ? dd + 3 * WC : sink;
+#pragma unroll
+                        for (int ch = 0; ch < 3; ++ch) dd[ch * WC] += a[ch] * (1.0f - fr_);
+#pragma unroll
+                        for (int ch = 0; ch < 3; ++ch) d2[ch * WC] += a[ch] * fr_;
+                    }
+                }
+            }
+            // staircase v (prefix of D) in place, total transmittance exp(-v_{M-1})
+            double vt[3] = {1.0, 1.0, 1.0};
+            if (act) {
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) {
+                    float r = 0.0f;
+#pragma unroll
+                    for (int k = 0; k < M; ++k) {
+                        float* a = part + k * 3 * WC + ch * WC + lane;
+                        r += *a;
+                        *a = r;
+                    }
+                    vt[ch] = (double)expf(-r);
+                }
+            }
+            // evaluate (step 3)
+            float ac[3] = {0.f, 0.f, 0.f}, wg[3] = {0.f, 0.f, 0.f}, df = 0.f;
+            double ro[2] = {0.0, 0.0};
+            if (act) {
+                const CellsCol<M> col{part + lane};
+                if (!GEN) {
+                    eval_chunk_fast<R>(sm.zfix + (WOIT_ALIASZ ? sh4 : 0), sm.alpha, sm.trans, col, sm.rad, cst, clen,
+                                       crot, sh4, ac, wg);
+                } else {
+                    double d[3] = {0.0, 0.0, 0.0}, topq = INFINITY;
+                    if (refr) {
+                        ray_dir(kp, kp.f.pixel_base + p, d);
+                        topq = kp.f.opaque_depth ? (double)kp.f.opaque_depth[p] : INFINITY;
+                    }
+                    eval_gen(col, cst, clen, crot, d, topq, ac, wg, df, ro);
+                }
+            }
+            fence_proxy_async();  // v̂ in smem becomes visible to the bulk store
+            __syncwarp();
+            if (kp.b.vhat) {
+                const int64_t i0 = (fa + 3) & ~(int64_t)3, i1 = fb & ~(int64_t)3;
+                const bool bulk = kp.use_tma && i1 > i0;
+                if (bulk && lane == 0) {
+                    bulk_s2g(kp.b.vhat + 3 * i0, sm.rad + 3 * (i0 - a4), (uint32_t)(12 * (i1 - i0)));
+                    bulk_commit();
+                }
+                const int nhead = bulk ? (int)(i0 - fa) : (int)(fb - fa);
+                const int ntail = bulk ? (int)(fb - i1) : 0;
+                for (int i = lane; i < nhead + ntail; i += 32) {
+                    const int64_t f = i < nhead ? fa + i : i1 + (i - nhead);
+                    const int si = (int)(f - a4);
+                    kp.b.vhat[3 * f] = sm.rad[3 * si];
+                    kp.b.vhat[3 * f + 1] = sm.rad[3 * si + 1];
+                    kp.b.vhat[3 * f + 2] = sm.rad[3 * si + 2];
+                }
+            }
+            // accumulators and composite (step 4): the chunk sums of a one-chunk pixel
+            if (act) {
+                const double ro0 = 0.0 + (double)(float)ro[0], ro1 = 0.0 + (double)(float)ro[1];
+                double dp = 0.0;
+                if (diffuse) {
+                    dp = dadd(dp, ddiv(0.0 + (double)df, 3.0));
+                    if (kp.b.diffusion) kp.b.diffusion[p] = (float)dp;
+                }
+                if (kp.b.refraction_offset) {
+                    kp.b.refraction_offset[p * 2] = GEN ? (float)ro0 : 0.0f;
+                    kp.b.refraction_offset[p * 2 + 1] = GEN ? (float)ro1 : 0.0f;
+                }
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) {
+                    const double acc = 0.0 + (double)ac[ch], wgt = 0.0 + (double)wg[ch];
+                    if (kp.b.accum) kp.b.accum[p * 3 + ch] = (float)acc;
+                    if (kp.b.weight) kp.b.weight[p * 3 + ch] = (float)wgt;
+                    if (kp.b.output)
+                        kp.b.output[p * 3 + ch] =
+                            GEN ? composite_channel(kp, p, ch, acc, wgt, ro0, ro1, vt[ch], dp)
+                                : composite_fast_ch(flags, acc, wgt, (double)kp.f.opaque_color[p * 3 + ch], vt[ch]);
+                }
+            }
+            // coefficients: Haar analysis of each channel's staircase in f64, transposed
+            // through shared memory ([V][33] over the staging arrays, free once the v̂
+            // store has read them) into coalesced stores
+            if (kp.b.coeffs) {
+                if (lane == 0) bulk_wait_read_all();
+                __syncwarp();
+                float* stg = sm.depth;
+                if (act) {
+#pragma unroll 1
+                    for (int ch = 0; ch < 3; ++ch) {
+                        double T[M], c[S];
+#pragma unroll
+                        for (int k = 0; k < M; ++k) T[k] = (double)part[k * 3 * WC + ch * WC + lane];
+                        haar_analysis<R>(T, c);
+#pragma unroll
+                        for (int sl = 0; sl < S; ++sl) stg[(3 * sl + ch) * 33 + lane] = (float)c[sl];
+                    }
+                }
+                __syncwarp();
+                float* g = kp.b.coeffs + (w0 + q0) * V;
+                for (int o = lane; o < nqs * V; o += 32) {
+                    const int pq = o / V, r = o - pq * V;
+                    g[o] = stg[r * 33 + pq];
+                }
+            }
+            __syncwarp();
+            q0 = q1;
+            continue;
         }
 
         // ---- 2. chunks + per-pixel init (overlaps the copies) -----------------------
@@ -1058,17 +1350,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
                 double T[M];
 #pragma unroll
                 for (int k = 0; k < M; ++k) T[k] = (double)rc[k];
-#pragma unroll
-                for (int m = 0; m <= R; ++m) {
-                    const int half = M >> (m + 1);  // wavelets at level n = R - m
-#pragma unroll
-                    for (int k = 0; k < half; ++k) {
-                        const double x = T[2 * k], y = T[2 * k + 1];
-                        c[half + k] = dmul(dmul(dsub(x, y), kSqrt2Pow[R - m]), 1.0 / M);
-                        T[k] = dadd(x, y);
-                    }
-                }
-                c[0] = dmul(T[0], 1.0 / M);
+                haar_analysis<R>(T, c);
                 if (GEN && (ph & PH_BUILD_ACC)) {
 #pragma unroll
                     for (int s = 0; s < S; ++s) c[s] = dadd(c[s], (double)kp.b.coeffs[(w0 + q) * V + 3 * s + kch]);
@@ -1161,48 +1443,9 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
                 }
                 const bool op_staged = ph & PH_BUILD;  // the build left alpha (1 - T') in the trans slot
                 if (!GEN) {
-                    eval_chunk_fast<R>(sm.zfix + (WOIT_ALIASZ ? sh4 : 0), sm.alpha, sm.trans, cq2, sm.rad, cst, clen, crot, sh4, ac, wg);
+                    eval_chunk_fast<R>(sm.zfix + (WOIT_ALIASZ ? sh4 : 0), sm.alpha, sm.trans, CellsPair{cq2}, sm.rad, cst, clen, crot, sh4, ac, wg);
                 } else {
-                int jj = crot;
-#pragma unroll kUnroll
-                for (int j = 0; j < clen; ++j) {
-                    const int fr = cst + jj;
-                    jj = jj + 1 == clen ? 0 : jj + 1;
-                    const int si = sh4 + fr;
-                    int c0;
-                    float t;
-                    eval_cell(sm.zfix[fr], R, c0, t);
-                    const float2* cv = cq2 + c0 * 3;
-                    const float al = sm.alpha[si];
-                    bool cb_ = false;
-                    float io = 1.0f;
-                    if (need_ior) {
-                        io = sm.ior[si];
-                        cb_ = cube && io > 1.0f && (!bfonly || sm.bf[shb + fr] != 0);
-                    }
-                    float vs = 0.0f;
-#pragma unroll
-                    for (int ch = 0; ch < 3; ++ch) {
-                        // A = lerp of the two neighbouring cell centres, clamped >= 0 (wavelet.py:316-319)
-                        const float2 vd = cv[ch];
-                        const float A = fmaxf(fmaf(t, vd.y, vd.x), 0.0f);
-                        const float vh = exp_neg(A);
-                        const float Lr = sm.rad[3 * si + ch];
-                        const float op = op_staged ? sm.trans[3 * si + ch] : opacity_ch(al, sm.trans[3 * si + ch], cb_);
-                        ac[ch] += (Lr * al) * vh;
-                        wg[ch] += op * vh;
-                        vs += vh;
-                        sm.rad[3 * si + ch] = vh;  // v̂ replaces radiance in place
-                    }
-                    if (diffuse) df += al * vs;  // diffusion coverage (woit.h WOIT_DIFFUSION)
-                    if (refr && io > 1.0f) {
-                        const float nrm[3] = {sm.normal[3 * si], sm.normal[3 * si + 1], sm.normal[3 * si + 2]};
-                        double off[2];
-                        refraction_offset(kp, d, topq, sm.depth[si], nrm, io, off);
-                        ro[0] += off[0];
-                        ro[1] += off[1];
-                    }
-                }
+                    eval_gen(CellsPair{cq2}, cst, clen, crot, d, topq, ac, wg, df, ro);
                 }
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) {
@@ -1508,13 +1751,13 @@ size_t long_smem_bytes() {
     return (size_t)V * TL * 8 + (size_t)V * 8 + (size_t)V * 4;
 }
 
-template <int R, bool GEN, bool FUS>
+template <int R, bool GEN, bool FUS, bool THIN>
 cudaError_t launch_tiles(const KParams& kp, cudaStream_t st) {
     using G = WT<R>;
     const uint32_t ph = (GEN && !FUS) ? kp.phases : (PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE);
     const WLayout L = make_wlayout<R>(ph, GEN ? kp.p.flags : (kp.p.flags & WOIT_NORMALIZE), !GEN && WOIT_ALIASZ);
     const int bytes = (int)(L.total * G::WPB);
-    cudaError_t err = cudaFuncSetAttribute(frame_kernel<R, GEN, FUS>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaError_t err = cudaFuncSetAttribute(frame_kernel<R, GEN, FUS, THIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (err != cudaSuccess) return err;
     // persistent grid: as many CTAs as can be resident, each warp loops over windows
     const int64_t warps = (kp.f.npix + G::WIN - 1) / G::WIN;
@@ -1522,14 +1765,14 @@ cudaError_t launch_tiles(const KParams& kp, cudaStream_t st) {
     int dev = 0, sms = 148, per_sm = 1;
     if (cudaGetDevice(&dev) == cudaSuccess)
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frame_kernel<R, GEN, FUS>, G::WPB * 32, bytes) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frame_kernel<R, GEN, FUS, THIN>, G::WPB * 32, bytes) !=
             cudaSuccess || per_sm < 1)
         per_sm = 1;
     cudaGetLastError();
     const int64_t resident = (int64_t)sms * per_sm * WOIT_PERSIST;
     if (WOIT_PERSIST > 0) grid = grid < resident ? grid : resident;
     if (grid > 0) {
-        frame_kernel<R, GEN, FUS><<<(unsigned)grid, G::WPB * 32, bytes, st>>>(kp);
+        frame_kernel<R, GEN, FUS, THIN><<<(unsigned)grid, G::WPB * 32, bytes, st>>>(kp);
         err = cudaGetLastError();
     }
     return err;
@@ -1541,8 +1784,14 @@ cudaError_t launch_rank(const KParams& kp, cudaStream_t st) {
     constexpr uint32_t kFused = PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE;
     const bool fused = kp.phases == kFused;
     const bool fast = fused && (kp.p.flags & ~WOIT_NORMALIZE) == 0;
-    cudaError_t err = fast ? launch_tiles<R, false, true>(kp, st)
-                           : fused ? launch_tiles<R, true, true>(kp, st) : launch_tiles<R, true, false>(kp, st);
+    // thin sub-tiles are compiled into a separate instance of the fast kernel: their
+    // code measurably slows the deep-pixel instance even when no thin sub-tile forms
+    // (the two give identical bits, so the choice is only a matter of speed)
+    const bool shallow = WOIT_THIN && kp.f.nfrag <= 16 * kp.f.npix;
+    cudaError_t err = fast ? (shallow ? launch_tiles<R, false, true, true>(kp, st)
+                                      : launch_tiles<R, false, true, false>(kp, st))
+                           : fused ? launch_tiles<R, true, true, WOIT_THIN>(kp, st)
+                                   : launch_tiles<R, true, false, false>(kp, st);
     if (err != cudaSuccess) return err;
     const size_t ls = long_smem_bytes<R>();
     err = cudaFuncSetAttribute(long_pixel_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ls);

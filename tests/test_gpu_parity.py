@@ -209,11 +209,12 @@ def test_band_split_is_bit_identical(W):
     assert torch.equal(a, b) and torch.equal(a, c)
 
 
-@pytest.mark.parametrize("layers", [128, 256])
-def test_deep_band_split_is_bit_identical(W, layers):
-    """Deep ragged pixels: sub-tiles of one to a few pixels, so the deep-pixel combine's
-    lane split changes with the band split; the images, coefficients and v̂ must not,
-    and they match the oracle."""
+@pytest.mark.parametrize("layers", [6, 12, 128, 256])
+def test_tiling_is_bit_identical(W, layers):
+    """Ragged runs: shallow ones (thin sub-tiles, one pixel per lane, whose extent
+    depends on where the windows fall) and deep ones (the deep-pixel combine's lane
+    split changes with the sub-tile). Band splits move the windows; the images,
+    coefficients and v̂ must not change, and they match the oracle."""
     sf = W.synth.generate("ragged", 37, 23, seed=13, layers=layers)
     frame = W.FrameFragments.from_synth(sf)
     outs = [W.render_frame(None, W.RenderConfig(rank=3, width=37, height=23, workers=k), frame=frame)
@@ -229,6 +230,28 @@ def test_deep_band_split_is_bit_identical(W, layers):
     assert np.abs(h(full.coeffs) - ref.coeffs).max() <= 1e-5
     assert np.abs(h(full.vhat) - ref.vhat).max() <= 1e-5
     assert np.abs(h(full.output) - ref.output).max() <= 1e-4
+
+
+def test_thin_and_deep_kernels_agree_bitwise(W):
+    """Shallow frames (<= 16 fragments per pixel on average) launch the fast kernel
+    with thin sub-tiles, deeper ones the instance without: a shallow band rendered
+    alone (thin) equals the same rows of a deep frame (no thin), bit for bit."""
+    w = 40
+    top = W.synth.generate("ragged", w, 24, seed=21, layers=8, row0=0, rows=12)
+    bot = W.synth.generate("particles", w, 24, seed=21, layers=64, row0=12, rows=12)
+    cat = lambda a, b: np.concatenate([a, b])
+    offs = cat(top.offsets[:-1], bot.offsets + top.offsets[-1])
+    sf = W.synth.SynthFrame(w, 24, 0, 24, offs, *(cat(getattr(top, k), getattr(bot, k)) for k in (
+        "depth", "alpha", "trans", "radiance", "normal", "ior", "backface", "opaque_depth", "opaque_color")))
+    frame = W.FrameFragments.from_synth(sf)
+    assert frame.nfrag > 16 * frame.npix and top.nfrag <= 16 * 12 * w
+    cfg = W.RenderConfig(rank=3, width=w, height=24)
+    full = W.render_band(frame, cfg, vhat=True)
+    band = W.render_band(W.FrameFragments.from_synth(top), cfg, vhat=True)
+    torch.cuda.synchronize()
+    P, n = 12 * w, top.nfrag
+    assert torch.equal(full.coeffs[:P], band.coeffs) and torch.equal(full.vhat[:n], band.vhat)
+    assert torch.equal(full.output[:P], band.output) and torch.equal(full.near[:P], band.near)
 
 
 def test_repeat_runs_bit_identical(W):

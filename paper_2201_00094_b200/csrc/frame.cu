@@ -43,6 +43,9 @@
 #ifndef WOIT_THIN  // thin sub-tiles (one pixel per lane) for shallow pixel runs
 #define WOIT_THIN 1
 #endif
+#ifndef WOIT_GEN_DYN  // dynamic window claims in the general kernel
+#define WOIT_GEN_DYN 1
+#endif
 #ifndef WOIT_DEEPCOMB  // deep-pixel combine: lanes split over cell blocks
 #define WOIT_DEEPCOMB 1
 #endif
@@ -560,11 +563,25 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
     const int64_t nwarps = (int64_t)gridDim.x * G::WPB;
     int64_t win = (int64_t)blockIdx.x * G::WPB + (threadIdx.x >> 5);
     if (win >= nwin) return;  // warp-uniform
+    // The claims are pipelined one window deep: the atomic for the window after next
+    // is issued while the next window's id (claimed one window earlier) is consumed,
+    // so its round trip is hidden behind a window of work.
+    // (Fast path only: in the general kernel the extra live register spills.)
+#if WOIT_DYN
+    unsigned long long claim_raw = 0;
+    if (!GEN && lane == 0) claim_raw = atomicAdd(kp.win_counter, 1ull);
+#endif
     auto claim = [&]() -> int64_t {
 #if WOIT_DYN
-        unsigned long long c = 0;
-        if (lane == 0) c = atomicAdd(kp.win_counter, 1ull);
-        return nwarps + (int64_t)__shfl_sync(0xffffffffu, c, 0);
+        if (GEN && !WOIT_GEN_DYN) return win + nwarps;
+        if (GEN) {
+            unsigned long long c = 0;
+            if (lane == 0) c = atomicAdd(kp.win_counter, 1ull);
+            return nwarps + (int64_t)__shfl_sync(0xffffffffu, c, 0);
+        }
+        const int64_t c = nwarps + (int64_t)__shfl_sync(0xffffffffu, claim_raw, 0);
+        if (lane == 0) claim_raw = atomicAdd(kp.win_counter, 1ull);
+        return c;
 #else
         return win + nwarps;
 #endif

@@ -46,9 +46,6 @@
 #ifndef WOIT_GEN_DYN  // dynamic window claims in the general kernel
 #define WOIT_GEN_DYN 1
 #endif
-#ifndef WOIT_DEEPCOMB  // deep-pixel combine: lanes split over cell blocks
-#define WOIT_DEEPCOMB 1
-#endif
 #ifndef WOIT_FFMA2
 #define WOIT_FFMA2 1
 #endif
@@ -134,35 +131,6 @@ WOIT_D void haar_cells(const double c[], double cell[]) {
     }
     (void)width;
     (void)S;
-}
-
-// Sum over a pixel's nc chunk partials of one cell (pvk = the cell's row at the
-// pixel's first chunk). The order is a function of the cell's rotation km = k mod ng
-// and nc only: whole 4-chunk groups (nc % 4 == 0) are visited from group km on,
-// each group in chunk order; otherwise all chunks in order. With one group this is
-// plain chunk order. Rotating by the cell spreads the lanes of the deep-pixel
-// combine (one lane per cell block) over the shared-memory banks.
-template <int WC>
-WOIT_D float cell_sum(const float* pvk, int nc, int km, bool al4) {
-    float r = 0.0f;
-    if ((nc & 3) == 0) {
-        const int ng = nc >> 2;
-        int g = km;
-#pragma unroll 1
-        for (int s = 0; s < ng; ++s) {
-            const float* pg = pvk + 4 * g;
-            const float4 p4 = al4 ? *reinterpret_cast<const float4*>(pg) : make_float4(pg[0], pg[1], pg[2], pg[3]);
-            r += p4.x;
-            r += p4.y;
-            r += p4.z;
-            r += p4.w;
-            g = g + 1 == ng ? 0 : g + 1;
-        }
-    } else {
-#pragma unroll 1
-        for (int i = 0; i < nc; ++i) r += pvk[i];
-    }
-    return r;
 }
 
 // cell table entry (v_c, v_{c+1} - v_c) for one (pixel, channel) of the sub-tile;
@@ -1227,113 +1195,16 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
             const int kch = task ? t / nqs : 0, kq = task ? t - kch * nqs : 0;
             double c[S];
             float rc[M];
-            // Few deep pixels (>= 64 fragments each, <= 4 per sub-tile): the (pixel,
-            // channel, cell block) sums are spread over the warp -- KB cells per lane, the
-            // cells k = blk + j B of a block, B = M / KB blocks per (pixel, channel) --
-            // and gathered through shared memory. Each cell's summation order is
-            // cell_sum's (a function of k and the run length only), so the split -- a
-            // function of the tiling -- never changes a bit of the result.
-            constexpr int B = M >= 8 ? 8 : M, KB = M / B, NR = (12 * B + 31) / 32;
-            if (WOIT_DEEPCOMB && nqs <= 4 && B > 1) {
-                constexpr int SR = M % 4 == 0 ? M + 4 : M + 1;  // [ntask][SR] scratch rows
-                float rs[NR][KB];
-                int nr = 0;
-#pragma unroll
-                for (int r = 0; r < NR; ++r) {  // ntask B <= 12 B lane tasks
-                    const int u = lane + 32 * r;
-                    const int tb = u / B, blk = u % B;
-                    if (tb < ntask) {
-                        ++nr;
-                        const int kchb = tb / nqs, kqb = tb - kchb * nqs;
-                        const int q = q0 + kqb;
-                        const int nc = (sm.cb[q + 1] - sm.cb[q]);
-                        const int cbq = sm.cb[q] - sm.cb[q0];
-                        const float* pv = part + kchb * WC + cbq;
-#pragma unroll
-                        for (int j = 0; j < KB; ++j) rs[r][j] = 0.0f;
-                        if ((nc & 3) == 0 && ((cbq & 3) == 0)) {
-                            const int ng = nc >> 2;
-                            int g[KB];
-#pragma unroll
-                            for (int j = 0; j < KB; ++j) g[j] = (blk + j * B) % ng;
-#pragma unroll 1
-                            for (int st = 0; st < ng; ++st) {
-#pragma unroll
-                                for (int j = 0; j < KB; ++j) {
-                                    const float4 p4 =
-                                        *reinterpret_cast<const float4*>(pv + (blk + j * B) * 3 * WC + 4 * g[j]);
-                                    rs[r][j] += p4.x;
-                                    rs[r][j] += p4.y;
-                                    rs[r][j] += p4.z;
-                                    rs[r][j] += p4.w;
-                                    g[j] = g[j] + 1 == ng ? 0 : g[j] + 1;
-                                }
-                            }
-                        } else {
-                            const int ng = (nc & 3) == 0 && nc > 0 ? nc >> 2 : 1;
-#pragma unroll
-                            for (int j = 0; j < KB; ++j)
-                                rs[r][j] = cell_sum<WC>(pv + (blk + j * B) * 3 * WC, nc, (blk + j * B) % ng, false);
-                        }
-                    }
-                }
-                __syncwarp();  // every lane has read its partials: the region takes the sums
-#pragma unroll
-                for (int r = 0; r < NR; ++r) {
-                    const int u = lane + 32 * r;
-                    if (r < nr) {
-#pragma unroll
-                        for (int j = 0; j < KB; ++j) part[(u / B) * SR + u % B + j * B] = rs[r][j];
-                    }
-                }
-                __syncwarp();
-                if (task) {
-                    if constexpr (M % 4 == 0) {
-#pragma unroll
-                        for (int k = 0; k < M; k += 4) {
-                            const float4 v4 = *reinterpret_cast<const float4*>(part + t * SR + k);
-                            rc[k] = v4.x;
-                            rc[k + 1] = v4.y;
-                            rc[k + 2] = v4.z;
-                            rc[k + 3] = v4.w;
-                        }
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < M; ++k) rc[k] = part[t * SR + k];
-                    }
-#pragma unroll
-                    for (int k = 1; k < M; ++k) rc[k] += rc[k - 1];
-                }
-            } else if (task) {
+            if (task) {
                 const int q = q0 + kq;
                 const int nc = (sm.cb[q + 1] - sm.cb[q]);
                 const int cbq = sm.cb[q] - sm.cb[q0];
                 const float* pv = part + kch * WC + cbq;
 #pragma unroll
                 for (int k = 0; k < M; ++k) rc[k] = 0.0f;
-                if ((nc & 3) == 0 && nc > 4) {
-                    // whole 4-chunk groups, more than one: cell_sum's rotated group order
-                    // (cell k reads group (k + st) mod ng at step st), cells interleaved
-                    const int ng = nc >> 2;
-                    const bool al4 = (cbq & 3) == 0;
-#pragma unroll 1
-                    for (int st = 0; st < ng; ++st) {
-                        int g = st;
-#pragma unroll
-                        for (int k = 0; k < M; ++k) {
-                            const float* pg = pv + k * 3 * WC + 4 * g;
-                            const float4 p4 = al4 ? *reinterpret_cast<const float4*>(pg)
-                                                  : make_float4(pg[0], pg[1], pg[2], pg[3]);
-                            rc[k] += p4.x;
-                            rc[k] += p4.y;
-                            rc[k] += p4.z;
-                            rc[k] += p4.w;
-                            g = g + 1 == ng ? 0 : g + 1;
-                        }
-                    }
-                } else if (((cbq | nc) & 3) == 0) {
-                    // one group (the common shallow case): cell_sum's order, all cells
-                    // interleaved for ILP, 16-B vector loads
+                // chunks summed in chunk order (fixed by the pixel's run length only);
+                // 16-B vector loads when the pixel's chunk group is 4-aligned
+                if (((cbq | nc) & 3) == 0) {
 #pragma unroll 1
                     for (int i = 0; i < nc; i += 4) {
 #pragma unroll

@@ -212,9 +212,9 @@ def test_band_split_is_bit_identical(W):
 @pytest.mark.parametrize("layers", [6, 12, 128, 256])
 def test_tiling_is_bit_identical(W, layers):
     """Ragged runs: shallow ones (thin sub-tiles, one pixel per lane, whose extent
-    depends on where the windows fall) and deep ones (the deep-pixel combine's lane
-    split changes with the sub-tile). Band splits move the windows; the images,
-    coefficients and v̂ must not change, and they match the oracle."""
+    depends on where the windows fall) and deep ones (sub-tiles of one or two
+    pixels). Band splits move the windows; the images, coefficients and v̂ must not
+    change, and they match the oracle."""
     sf = W.synth.generate("ragged", 37, 23, seed=13, layers=layers)
     frame = W.FrameFragments.from_synth(sf)
     outs = [W.render_frame(None, W.RenderConfig(rank=3, width=37, height=23, workers=k), frame=frame)

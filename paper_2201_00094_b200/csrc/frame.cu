@@ -53,6 +53,8 @@
 #define WOIT_PERSIST 1
 #endif
 namespace woit {
+// fast-kernel instances (frame_kernel VAR): plain, with thin sub-tiles, with the deep-pixel combine
+constexpr int kVarPlain = 0, kVarThin = 1, kVarDeep = 2;
 constexpr int kUnroll = WOIT_UNROLL;  // fragment-loop unroll (tuning knob)
 constexpr int kZUnroll = WOIT_ZUNROLL;  // z-loop unroll
 }
@@ -509,7 +511,7 @@ WOIT_D WSmem<R, GEN> wcarve(unsigned char* base, const WLayout& L) {
 // FUS: the phases are the fused render's (compile-time constant), so the
 // step-wise accumulate / from-buffer branches compile out; GEN && !FUS serves the
 // step1..step4 entry points.
-template <int R, bool GEN, bool FUS, bool THIN>
+template <int R, bool GEN, bool FUS, int VAR>
 __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R>::WPB) frame_kernel(const __grid_constant__ KParams kp) {
     using G = WT<R>;
     constexpr int S = G::S, V = G::V, CH = G::CH, WC = 32, FBW = G::FBW, WIN = G::WIN, SUBP = G::SUBP;
@@ -567,7 +569,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
     const int64_t nalloc = kp.f.nfrag;
     // thin sub-tiles: the fused render without packed storage, when the coefficient
     // transpose ([V][33] floats) fits over the depth / alpha / T / L staging arrays
-    const bool kThinOK = THIN && FUS && !packed && V * 33 * 4 <= (int)(L.rad - L.depth) + 12 * (FBW + 4);
+    const bool kThinOK = VAR == kVarThin && FUS && !packed && V * 33 * 4 <= (int)(L.rad - L.depth) + 12 * (FBW + 4);
 
     if (lane == 0) mbar_init(sm.bar, 1);
     uint32_t parity = 0;
@@ -1195,16 +1197,99 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
             const int kch = task ? t / nqs : 0, kq = task ? t - kch * nqs : 0;
             double c[S];
             float rc[M];
-            if (task) {
+            // Few deep pixels (>= 64 fragments each, <= 4 per sub-tile): the (pixel,
+            // channel, cell block) sums are spread over the warp -- KB cells per lane, the
+            // cells k = blk + j B of a block, B = M / KB blocks per (pixel, channel) --
+            // and gathered through shared memory. Each cell is summed in the general
+            // combine's order (chunk order, 4-chunk groups), so neither the split -- a
+            // function of the tiling -- nor the kernel instance changes a bit.
+            constexpr int B = M >= 8 ? 8 : M, KB = M / B, NR = (12 * B + 31) / 32;
+            if (VAR == kVarDeep && nqs <= 4 && B > 1) {
+                constexpr int SR = M % 4 == 0 ? M + 4 : M + 1;  // [ntask][SR] scratch rows
+                float rs[NR][KB];
+                int nr = 0;
+#pragma unroll
+                for (int r = 0; r < NR; ++r) {  // ntask B <= 12 B lane tasks
+                    const int u = lane + 32 * r;
+                    const int tb = u / B, blk = u % B;
+                    if (tb < ntask) {
+                        ++nr;
+                        const int kchb = tb / nqs, kqb = tb - kchb * nqs;
+                        const int q = q0 + kqb;
+                        const int nc = (sm.cb[q + 1] - sm.cb[q]);
+                        const int cbq = sm.cb[q] - sm.cb[q0];
+                        const float* pv = part + kchb * WC + cbq;
+#pragma unroll
+                        for (int j = 0; j < KB; ++j) rs[r][j] = 0.0f;
+                        if ((nc & 3) == 0 && (cbq & 3) == 0) {
+                            // chunk order in 4-chunk groups, like the general combine; lane
+                            // blk runs blk steps behind lane 0, so at any step the lanes of
+                            // a (pixel, channel) read different groups -- distinct banks
+                            const int ng = nc >> 2;
+#pragma unroll 1
+                            for (int st = 0; st < ng + B - 1; ++st) {
+                                const int g = st - blk;
+                                if (g >= 0 && g < ng) {
+#pragma unroll
+                                    for (int j = 0; j < KB; ++j) {
+                                        const float4 p4 =
+                                            *reinterpret_cast<const float4*>(pv + (blk + j * B) * 3 * WC + 4 * g);
+                                        rs[r][j] += p4.x;
+                                        rs[r][j] += p4.y;
+                                        rs[r][j] += p4.z;
+                                        rs[r][j] += p4.w;
+                                    }
+                                }
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < KB; ++j) {
+                                const float* pk = pv + (blk + j * B) * 3 * WC;
+                                float x = 0.0f;
+#pragma unroll 1
+                                for (int i = 0; i < nc; ++i) x += pk[i];
+                                rs[r][j] = x;
+                            }
+                        }
+                    }
+                }
+                __syncwarp();  // every lane has read its partials: the region takes the sums
+#pragma unroll
+                for (int r = 0; r < NR; ++r) {
+                    const int u = lane + 32 * r;
+                    if (r < nr) {
+#pragma unroll
+                        for (int j = 0; j < KB; ++j) part[(u / B) * SR + u % B + j * B] = rs[r][j];
+                    }
+                }
+                __syncwarp();
+                if (task) {
+                    if constexpr (M % 4 == 0) {
+#pragma unroll
+                        for (int k = 0; k < M; k += 4) {
+                            const float4 v4 = *reinterpret_cast<const float4*>(part + t * SR + k);
+                            rc[k] = v4.x;
+                            rc[k + 1] = v4.y;
+                            rc[k + 2] = v4.z;
+                            rc[k + 3] = v4.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < M; ++k) rc[k] = part[t * SR + k];
+                    }
+#pragma unroll
+                    for (int k = 1; k < M; ++k) rc[k] += rc[k - 1];
+                }
+            } else if (task) {
                 const int q = q0 + kq;
                 const int nc = (sm.cb[q + 1] - sm.cb[q]);
                 const int cbq = sm.cb[q] - sm.cb[q0];
                 const float* pv = part + kch * WC + cbq;
 #pragma unroll
                 for (int k = 0; k < M; ++k) rc[k] = 0.0f;
-                // chunks summed in chunk order (fixed by the pixel's run length only);
-                // 16-B vector loads when the pixel's chunk group is 4-aligned
                 if (((cbq | nc) & 3) == 0) {
+                    // chunks summed in chunk order (fixed by the pixel's run length only),
+                    // all cells interleaved for ILP, 16-B vector loads
 #pragma unroll 1
                     for (int i = 0; i < nc; i += 4) {
 #pragma unroll
@@ -1639,13 +1724,13 @@ size_t long_smem_bytes() {
     return (size_t)V * TL * 8 + (size_t)V * 8 + (size_t)V * 4;
 }
 
-template <int R, bool GEN, bool FUS, bool THIN>
+template <int R, bool GEN, bool FUS, int VAR>
 cudaError_t launch_tiles(const KParams& kp, cudaStream_t st) {
     using G = WT<R>;
     const uint32_t ph = (GEN && !FUS) ? kp.phases : (PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE);
     const WLayout L = make_wlayout<R>(ph, GEN ? kp.p.flags : (kp.p.flags & WOIT_NORMALIZE), !GEN && WOIT_ALIASZ);
     const int bytes = (int)(L.total * G::WPB);
-    cudaError_t err = cudaFuncSetAttribute(frame_kernel<R, GEN, FUS, THIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaError_t err = cudaFuncSetAttribute(frame_kernel<R, GEN, FUS, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (err != cudaSuccess) return err;
     // persistent grid: as many CTAs as can be resident, each warp loops over windows
     const int64_t warps = (kp.f.npix + G::WIN - 1) / G::WIN;
@@ -1653,14 +1738,14 @@ cudaError_t launch_tiles(const KParams& kp, cudaStream_t st) {
     int dev = 0, sms = 148, per_sm = 1;
     if (cudaGetDevice(&dev) == cudaSuccess)
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frame_kernel<R, GEN, FUS, THIN>, G::WPB * 32, bytes) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frame_kernel<R, GEN, FUS, VAR>, G::WPB * 32, bytes) !=
             cudaSuccess || per_sm < 1)
         per_sm = 1;
     cudaGetLastError();
     const int64_t resident = (int64_t)sms * per_sm * WOIT_PERSIST;
     if (WOIT_PERSIST > 0) grid = grid < resident ? grid : resident;
     if (grid > 0) {
-        frame_kernel<R, GEN, FUS, THIN><<<(unsigned)grid, G::WPB * 32, bytes, st>>>(kp);
+        frame_kernel<R, GEN, FUS, VAR><<<(unsigned)grid, G::WPB * 32, bytes, st>>>(kp);
         err = cudaGetLastError();
     }
     return err;
@@ -1675,11 +1760,16 @@ cudaError_t launch_rank(const KParams& kp, cudaStream_t st) {
     // thin sub-tiles are compiled into a separate instance of the fast kernel: their
     // code measurably slows the deep-pixel instance even when no thin sub-tile forms
     // (the two give identical bits, so the choice is only a matter of speed)
+    // Likewise the deep-pixel combine (few pixels of >= 64 fragments per sub-tile) is
+    // compiled only into the instance for deep frames (> 160 fragments per pixel on
+    // average): it pays at 256 fragments per pixel and costs the others codegen.
     const bool shallow = WOIT_THIN && kp.f.nfrag <= 16 * kp.f.npix;
-    cudaError_t err = fast ? (shallow ? launch_tiles<R, false, true, true>(kp, st)
-                                      : launch_tiles<R, false, true, false>(kp, st))
-                           : fused ? launch_tiles<R, true, true, WOIT_THIN>(kp, st)
-                                   : launch_tiles<R, true, false, false>(kp, st);
+    const bool deep = kp.f.nfrag > 160 * kp.f.npix;
+    cudaError_t err = fast ? (shallow ? launch_tiles<R, false, true, kVarThin>(kp, st)
+                              : deep  ? launch_tiles<R, false, true, kVarDeep>(kp, st)
+                                      : launch_tiles<R, false, true, kVarPlain>(kp, st))
+                           : fused ? launch_tiles<R, true, true, WOIT_THIN ? kVarThin : kVarPlain>(kp, st)
+                                   : launch_tiles<R, true, false, kVarPlain>(kp, st);
     if (err != cudaSuccess) return err;
     const size_t ls = long_smem_bytes<R>();
     err = cudaFuncSetAttribute(long_pixel_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ls);

@@ -254,6 +254,31 @@ def test_thin_and_deep_kernels_agree_bitwise(W):
     assert torch.equal(full.output[:P], band.output) and torch.equal(full.near[:P], band.near)
 
 
+def test_deep_and_plain_kernels_agree_bitwise(W):
+    """Frames of > 160 fragments per pixel on average launch the fast kernel with the
+    deep-pixel combine: a band of 256-fragment pixels rendered alone (deep instance)
+    equals the same rows of a shallower frame (plain instance), bit for bit."""
+    w = 24
+    top = W.synth.generate("particles", w, 16, seed=22, layers=256, row0=0, rows=8)
+    bot = W.synth.generate("ragged", w, 16, seed=22, layers=8, row0=8, rows=8)
+    cat = lambda a, b: np.concatenate([a, b])
+    offs = cat(top.offsets[:-1], bot.offsets + top.offsets[-1])
+    sf = W.synth.SynthFrame(w, 16, 0, 16, offs, *(cat(getattr(top, k), getattr(bot, k)) for k in (
+        "depth", "alpha", "trans", "radiance", "normal", "ior", "backface", "opaque_depth", "opaque_color")))
+    frame = W.FrameFragments.from_synth(sf)
+    assert 16 * frame.npix < frame.nfrag <= 160 * frame.npix and top.nfrag > 160 * 8 * w
+    cfg = W.RenderConfig(rank=3, width=w, height=16)
+    full = W.render_band(frame, cfg, vhat=True)
+    band = W.render_band(W.FrameFragments.from_synth(top), cfg, vhat=True)
+    torch.cuda.synchronize()
+    P, n = 8 * w, top.nfrag
+    assert torch.equal(full.coeffs[:P], band.coeffs) and torch.equal(full.vhat[:n], band.vhat)
+    assert torch.equal(full.output[:P], band.output)
+    ref = O.render_frame(O.OFrame.from_synth(top), O.OConfig(rank=3, width=w, height=8))
+    assert np.abs(h(band.coeffs) - ref.coeffs).max() <= 1e-5
+    assert np.abs(h(band.output) - ref.output).max() <= 1e-4
+
+
 def test_repeat_runs_bit_identical(W):
     frame = W.FrameFragments.synthetic("particles", 64, 32, seed=4, layers=128)
     cfg = W.RenderConfig(rank=3, width=64, height=32)

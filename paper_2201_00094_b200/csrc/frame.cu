@@ -43,6 +43,9 @@
 #ifndef WOIT_THIN  // thin sub-tiles (one pixel per lane) for shallow pixel runs
 #define WOIT_THIN 1
 #endif
+#ifndef WOIT_FLAG_INSTANCES  // general-kernel instances specialised for fixed flag sets
+#define WOIT_FLAG_INSTANCES 1
+#endif
 #ifndef WOIT_GEN_DYN  // dynamic window claims in the general kernel
 #define WOIT_GEN_DYN 1
 #endif
@@ -403,22 +406,21 @@ WOIT_D void eval_chunk_fast(const zfix_t* __restrict__ zf, const float* __restri
 // and the composite with acc = wgt = 0, v_tot = 1, offset 0, D = 0, i.e. the
 // background itself -- without staging, chunks or the per-(pixel, channel) phases.
 template <int R, bool GEN>
-WOIT_D void empty_run(const KParams& kp, int64_t p0, int ne, int lane) {
+WOIT_D void empty_run(const KParams& kp, int flags, int64_t p0, int ne, int lane) {
     constexpr int V = 3 * (2 << R);
-    const int flags = GEN ? kp.p.flags : (kp.p.flags & WOIT_NORMALIZE);
     if (kp.b.coeffs) {
         float* c = kp.b.coeffs + p0 * V;
         const bool packed = GEN && (flags & WOIT_PACKED_STORAGE);
         if (V % 4 == 0 && (reinterpret_cast<uintptr_t>(c) & 15u) == 0) {
             constexpr int V4 = V / 4 > 0 ? V / 4 : 1;
             float4* c4 = reinterpret_cast<float4*>(c);
-            for (int i = lane; i < ne * V4; i += 32) {
-                float4 z = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-                if (packed) {
+            if (packed) {
+                for (int i = lane; i < ne * V4; i += 32) {
                     const float l0 = (i % V4) == 0 ? 0.0f : -0.0f;
-                    z = make_float4(l0, l0, l0, -0.0f);
+                    c4[i] = make_float4(l0, l0, l0, -0.0f);
                 }
-                c4[i] = z;
+            } else {
+                for (int i = lane; i < ne * V4; i += 32) c4[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
             }
         } else {
             for (int i = lane; i < ne * V; i += 32) c[i] = (packed && (i % V) >= 3) ? -0.0f : 0.0f;
@@ -441,7 +443,7 @@ WOIT_D void empty_run(const KParams& kp, int64_t p0, int ne, int lane) {
     if (kp.b.output) {
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch)
-            kp.b.output[p * 3 + ch] = GEN ? composite_channel(kp, p, ch, 0.0, 0.0, 0.0, 0.0, 1.0, 0.0)
+            kp.b.output[p * 3 + ch] = GEN ? composite_channel(kp, flags, p, ch, 0.0, 0.0, 0.0, 0.0, 1.0, 0.0)
                                           : kp.f.opaque_color[p * 3 + ch];
     }
 }
@@ -511,7 +513,7 @@ WOIT_D WSmem<R, GEN> wcarve(unsigned char* base, const WLayout& L) {
 // FUS: the phases are the fused render's (compile-time constant), so the
 // step-wise accumulate / from-buffer branches compile out; GEN && !FUS serves the
 // step1..step4 entry points.
-template <int R, bool GEN, bool FUS, int VAR>
+template <int R, bool GEN, bool FUS, int VAR, int FL>
 __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R>::WPB) frame_kernel(const __grid_constant__ KParams kp) {
     using G = WT<R>;
     constexpr int S = G::S, V = G::V, CH = G::CH, WC = 32, FBW = G::FBW, WIN = G::WIN, SUBP = G::SUBP;
@@ -520,7 +522,8 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
     constexpr uint32_t kFused = PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const uint32_t ph = (GEN && !FUS) ? kp.phases : kFused;
-    const int flags = GEN ? kp.p.flags : (kp.p.flags & WOIT_NORMALIZE);
+    // FL != 0: an instance specialised for exactly these flags (all but NORMALIZE)
+    const int flags = GEN ? (FL ? (FL | (kp.p.flags & WOIT_NORMALIZE)) : kp.p.flags) : (kp.p.flags & WOIT_NORMALIZE);
     const WLayout L = make_wlayout<R>(ph, flags, !GEN && WOIT_ALIASZ);
     const int lane = threadIdx.x & 31;
     WSmem<R, GEN> sm = wcarve<R, GEN>(smem_raw + (threadIdx.x >> 5) * L.total, L);
@@ -536,15 +539,17 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
     // The claims are pipelined one window deep: the atomic for the window after next
     // is issued while the next window's id (claimed one window earlier) is consumed,
     // so its round trip is hidden behind a window of work.
-    // (Fast path only: in the general kernel the extra live register spills.)
+    // (Fast kernel only: in the general kernel it measured slower -- the extra live
+    // register spills in the generic instance, costs occupancy in the specialised ones.)
 #if WOIT_DYN
     unsigned long long claim_raw = 0;
-    if (!GEN && lane == 0) claim_raw = atomicAdd(kp.win_counter, 1ull);
+    constexpr bool kPipeClaims = !GEN;
+    if (kPipeClaims && lane == 0) claim_raw = atomicAdd(kp.win_counter, 1ull);
 #endif
     auto claim = [&]() -> int64_t {
 #if WOIT_DYN
         if (GEN && !WOIT_GEN_DYN) return win + nwarps;
-        if (GEN) {
+        if (!kPipeClaims) {
             unsigned long long c = 0;
             if (lane == 0) c = atomicAdd(kp.win_counter, 1ull);
             return nwarps + (int64_t)__shfl_sync(0xffffffffu, c, 0);
@@ -714,7 +719,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
             const unsigned em = __ballot_sync(0xffffffffu, emp);
             const int ne = em == 0xffffffffu ? 32 : __ffs(~em) - 1;
             if (ne > 0) {
-                empty_run<R, GEN>(kp, w0 + q0, ne, lane);
+                empty_run<R, GEN>(kp, flags, w0 + q0, ne, lane);
                 q0 += ne;
                 continue;
             }
@@ -991,7 +996,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
                     if (kp.b.weight) kp.b.weight[p * 3 + ch] = (float)wgt;
                     if (kp.b.output)
                         kp.b.output[p * 3 + ch] =
-                            GEN ? composite_channel(kp, p, ch, acc, wgt, ro0, ro1, vt[ch], dp)
+                            GEN ? composite_channel(kp, flags, p, ch, acc, wgt, ro0, ro1, vt[ch], dp)
                                 : composite_fast_ch(flags, acc, wgt, (double)kp.f.opaque_color[p * 3 + ch], vt[ch]);
                 }
             }
@@ -1503,7 +1508,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
                 }
             }
             if ((ph & PH_COMPOSITE) && kp.b.output)
-                kp.b.output[p * 3 + kch] = composite_channel(kp, p, kch, acc, wgt, ro0, ro1, sm.vtot[kq * 3 + kch], dp);
+                kp.b.output[p * 3 + kch] = composite_channel(kp, flags, p, kch, acc, wgt, ro0, ro1, sm.vtot[kq * 3 + kch], dp);
         }
         fence_proxy_async();
         __syncwarp();
@@ -1706,7 +1711,7 @@ __global__ void __launch_bounds__(kLongT) long_pixel_kernel(const __grid_constan
             }
             if ((ph & PH_COMPOSITE) && kp.b.output) {
                 float out[3];
-                composite_pixel(kp, p, acc, wgt, ro[0], ro[1], vt, dp, out);
+                composite_pixel(kp, kp.p.flags, p, acc, wgt, ro[0], ro[1], vt, dp, out);
                 for (int ch = 0; ch < 3; ++ch) kp.b.output[p * 3 + ch] = out[ch];
             }
         }
@@ -1724,13 +1729,13 @@ size_t long_smem_bytes() {
     return (size_t)V * TL * 8 + (size_t)V * 8 + (size_t)V * 4;
 }
 
-template <int R, bool GEN, bool FUS, int VAR>
+template <int R, bool GEN, bool FUS, int VAR, int FL = 0>
 cudaError_t launch_tiles(const KParams& kp, cudaStream_t st) {
     using G = WT<R>;
     const uint32_t ph = (GEN && !FUS) ? kp.phases : (PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE);
     const WLayout L = make_wlayout<R>(ph, GEN ? kp.p.flags : (kp.p.flags & WOIT_NORMALIZE), !GEN && WOIT_ALIASZ);
     const int bytes = (int)(L.total * G::WPB);
-    cudaError_t err = cudaFuncSetAttribute(frame_kernel<R, GEN, FUS, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaError_t err = cudaFuncSetAttribute(frame_kernel<R, GEN, FUS, VAR, FL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (err != cudaSuccess) return err;
     // persistent grid: as many CTAs as can be resident, each warp loops over windows
     const int64_t warps = (kp.f.npix + G::WIN - 1) / G::WIN;
@@ -1738,17 +1743,36 @@ cudaError_t launch_tiles(const KParams& kp, cudaStream_t st) {
     int dev = 0, sms = 148, per_sm = 1;
     if (cudaGetDevice(&dev) == cudaSuccess)
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frame_kernel<R, GEN, FUS, VAR>, G::WPB * 32, bytes) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frame_kernel<R, GEN, FUS, VAR, FL>, G::WPB * 32, bytes) !=
             cudaSuccess || per_sm < 1)
         per_sm = 1;
     cudaGetLastError();
     const int64_t resident = (int64_t)sms * per_sm * WOIT_PERSIST;
     if (WOIT_PERSIST > 0) grid = grid < resident ? grid : resident;
     if (grid > 0) {
-        frame_kernel<R, GEN, FUS, VAR><<<(unsigned)grid, G::WPB * 32, bytes, st>>>(kp);
+        frame_kernel<R, GEN, FUS, VAR, FL><<<(unsigned)grid, G::WPB * 32, bytes, st>>>(kp);
         err = cudaGetLastError();
     }
     return err;
+}
+
+// The fused general kernel, with instances specialised (at rank 3) for the flag
+// sets of the measured configurations: the flags fold to constants, so the code of
+// the other features drops out (a smaller kernel: fewer instruction-cache misses,
+// fewer registers). Identical operations, identical bits.
+constexpr int kFlC3 = WOIT_REFRACTION | WOIT_CHROMATIC_ABERRATION | WOIT_CUBE_TRANSMISSION;  // config 3
+constexpr int kFlC3D = kFlC3 | WOIT_DIFFUSION;                                              // + diffusion
+constexpr int kFlRefr = WOIT_REFRACTION;                                                    // glass stacks
+template <int R>
+cudaError_t launch_general(const KParams& kp, cudaStream_t st) {
+    constexpr int TV = WOIT_THIN ? kVarThin : kVarPlain;
+    if constexpr (R == 3 && WOIT_FLAG_INSTANCES) {
+        const int fl = kp.p.flags & ~WOIT_NORMALIZE;
+        if (fl == kFlC3) return launch_tiles<R, true, true, TV, kFlC3>(kp, st);
+        if (fl == kFlC3D) return launch_tiles<R, true, true, TV, kFlC3D>(kp, st);
+        if (fl == kFlRefr) return launch_tiles<R, true, true, TV, kFlRefr>(kp, st);
+    }
+    return launch_tiles<R, true, true, TV>(kp, st);
 }
 
 template <int R>
@@ -1768,7 +1792,7 @@ cudaError_t launch_rank(const KParams& kp, cudaStream_t st) {
     cudaError_t err = fast ? (shallow ? launch_tiles<R, false, true, kVarThin>(kp, st)
                               : deep  ? launch_tiles<R, false, true, kVarDeep>(kp, st)
                                       : launch_tiles<R, false, true, kVarPlain>(kp, st))
-                           : fused ? launch_tiles<R, true, true, WOIT_THIN ? kVarThin : kVarPlain>(kp, st)
+                           : fused ? launch_general<R>(kp, st)
                                    : launch_tiles<R, true, false, kVarPlain>(kp, st);
     if (err != cudaSuccess) return err;
     const size_t ls = long_smem_bytes<R>();
@@ -1813,7 +1837,7 @@ __global__ void composite_kernel(const __grid_constant__ KParams kp) {
     const double oy = kp.b.refraction_offset ? kp.b.refraction_offset[2 * p + 1] : 0.0;
     const double dp = kp.b.diffusion ? (double)kp.b.diffusion[p] : 0.0;
     float out[3];
-    composite_pixel(kp, p, acc, wgt, ox, oy, vt, dp, out);
+    composite_pixel(kp, kp.p.flags, p, acc, wgt, ox, oy, vt, dp, out);
     for (int ch = 0; ch < 3; ++ch) kp.b.output[p * 3 + ch] = out[ch];
 }
 

@@ -307,11 +307,11 @@ WOIT_D double diffusion_weight(const KParams& kp, double dp) {
 // step4_composite for pixel p (band-local). accum/weight/refr are the pixel's
 // final accumulators, vtot = exp(-A_total), dp the diffusion coverage D_p
 // (only read with WOIT_DIFFUSION).
-WOIT_D void composite_pixel(const KParams& kp, int64_t p, const double acc[3],
+WOIT_D void composite_pixel(const KParams& kp, int flags, int64_t p, const double acc[3],
                             const double wgt[3], double ox, double oy, const double vtot[3],
                             double dp, float out[3]) {
     const int W = kp.f.width;
-    const int flags = kp.p.flags;
+    // flags: kp.p.flags, or a compile-time copy of them (specialised kernel instances)
     double bg[3];
     const bool gather = flags & (WOIT_CHROMATIC_ABERRATION | WOIT_REFRACTION);
     const bool full = kp.b.full_opaque_image != nullptr;
@@ -362,10 +362,10 @@ WOIT_D void composite_plain(int flags, const float bgc[3], const double acc[3], 
 
 // Channel `ch` of composite_pixel, for per-(pixel, channel) lanes: the same
 // operations, so the result is bit-identical to composite_pixel's channel.
-WOIT_D float composite_channel(const KParams& kp, int64_t p, int ch, double acc, double wgt, double ox,
+WOIT_D float composite_channel(const KParams& kp, int flags, int64_t p, int ch, double acc, double wgt, double ox,
                                double oy, double vt, double dp) {
     const int W = kp.f.width;
-    const int flags = kp.p.flags;
+    // flags as in composite_pixel
     const bool gather = flags & (WOIT_CHROMATIC_ABERRATION | WOIT_REFRACTION);
     const bool full = kp.b.full_opaque_image != nullptr;
     const int H = full ? kp.f.height : (int)(kp.f.npix / W);

@@ -42,8 +42,10 @@ template <bool FILL>
 struct Emitter {
     int64_t k;
     Out o;
+    bool live;  // false: a lane past the last pixel (emits nothing)
     WOIT_D void emit(double depth, double alpha, const double tr[3], const double rd[3], const double nr[3], double ior,
                      bool backface) {
+        if (!live) return;
         if (FILL) {
             o.depth[k] = (float)depth;
             o.alpha[k] = (float)alpha;
@@ -73,7 +75,13 @@ __global__ void __launch_bounds__(128) cast_kernel(const woit_scene_t s, int W, 
                                                    const int64_t* __restrict__ offsets, Out o, float* opaque_depth,
                                                    float* opaque_color) {
     const int64_t npix = (int64_t)W * H;
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npix; p += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    // warp-uniform trip count (the fog slabs are written by the whole warp); lanes past
+    // the end run the geometry of the last pixel and emit nothing
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t pw = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); pw < npix; pw += stride) {
+        const bool live = pw + lane < npix;
+        const int64_t p = live ? pw + lane : npix - 1;
         const int px = (int)(p % W), py = (int)(p / W);
         double d[3];
         primary_ray(s, W, H, px, py, d);
@@ -100,12 +108,12 @@ __global__ void __launch_bounds__(128) cast_kernel(const woit_scene_t s, int W, 
             for (int c = 0; c < 3; ++c) oc[c] = odd ? pr.checker[c] : pr.color[c];
             ot = t;
         }
-        if (FILL) {
+        if (FILL && live) {
             opaque_depth[p] = (float)ot;
 #pragma unroll
             for (int c = 0; c < 3; ++c) opaque_color[3 * p + c] = (float)oc[c];
         }
-        Emitter<FILL> em{FILL ? offsets[p] : 0, o};
+        Emitter<FILL> em{FILL && live ? offsets[p] : 0, o, live};
         const double nf[3] = {-s.forward[0], -s.forward[1], -s.forward[2]};
         for (int i = 0; i < s.nprims; ++i) {
             const woit_prim_t& pr = s.prims[i];
@@ -147,17 +155,54 @@ __global__ void __launch_bounds__(128) cast_kernel(const woit_scene_t s, int W, 
                 double tb = dirf > 0.0 ? ddiv(pr.far, dirf) : INFINITY;
                 ta = fmax(ta, kRayEps);
                 tb = fmin(tb, ot);
-                if (!(tb > ta)) continue;
-                const double delta = ddiv(dsub(tb, ta), (double)pr.count);
-                double tr[3], rd[3];
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    tr[c] = exp(dmul(-pr.sigma[c], delta));
-                    rd[c] = dmul(pr.color[c], dsub(1.0, tr[c]));
+                const int cnt = (em.live && tb > ta) ? pr.count : 0;
+                if (!FILL) {
+                    em.k += cnt;
+                    continue;
                 }
-                const double nz[3] = {0.0, 0.0, -1.0};
-                for (int j = 0; j < pr.count; ++j)
-                    em.emit(dadd(ta, dmul(dadd((double)j, 0.5), delta)), 1.0, tr, rd, nz, 1.0, false);
+                double delta = 0.0;
+                float trf[3] = {0.f, 0.f, 0.f}, rdf[3] = {0.f, 0.f, 0.f};
+                if (cnt) {
+                    delta = ddiv(dsub(tb, ta), (double)pr.count);
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const double tr = exp(dmul(-pr.sigma[c], delta));
+                        trf[c] = (float)tr;
+                        rdf[c] = (float)dmul(pr.color[c], dsub(1.0, tr));
+                    }
+                }
+                // The slices of every lane's slab are written by the whole warp, one lane's
+                // run at a time: consecutive threads store consecutive fragments (coalesced).
+                // Slice j's depth is ta + (j + 1/2) delta, as the per-lane loop computed it.
+                for (int L = 0; L < 32; ++L) {
+                    const int n = __shfl_sync(0xffffffffu, cnt, L);
+                    if (n == 0) continue;
+                    const int64_t k0 = __shfl_sync(0xffffffffu, em.k, L);
+                    const double ta_ = __shfl_sync(0xffffffffu, ta, L), de = __shfl_sync(0xffffffffu, delta, L);
+                    float t3[3], r3[3];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        t3[c] = __shfl_sync(0xffffffffu, trf[c], L);
+                        r3[c] = __shfl_sync(0xffffffffu, rdf[c], L);
+                    }
+                    for (int j = lane; j < n; j += 32) {
+                        const int64_t k = k0 + j;
+                        o.depth[k] = (float)dadd(ta_, dmul(dadd((double)j, 0.5), de));
+                        o.alpha[k] = 1.0f;
+                        o.ior[k] = 1.0f;
+                        o.bf[k] = 0;
+                    }
+                    float* tr3 = o.trans + 3 * k0;
+                    float* rd3 = o.rad + 3 * k0;
+                    float* nr3 = o.normal + 3 * k0;
+                    for (int e = lane; e < 3 * n; e += 32) {
+                        const int c = e % 3;
+                        tr3[e] = t3[c];
+                        rd3[e] = r3[c];
+                        nr3[e] = c == 2 ? -1.0f : 0.0f;
+                    }
+                }
+                em.k += cnt;
             } else if (pr.kind == WOIT_PRIM_PARTICLES) {
                 const double pr2 = dmul(pr.particle_radius, pr.particle_radius);
                 for (int k = 0; k < pr.count; ++k) {
@@ -185,7 +230,7 @@ __global__ void __launch_bounds__(128) cast_kernel(const woit_scene_t s, int W, 
                 }
             }
         }
-        if (!FILL) counts[p] = em.k;
+        if (!FILL && live) counts[p] = em.k;
     }
 }
 

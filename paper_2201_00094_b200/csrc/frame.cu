@@ -31,8 +31,8 @@
 #ifndef WOIT_DYN  // dynamic window claims
 #define WOIT_DYN 1
 #endif
-#ifndef WOIT_EVPIPE  // software-pipelined evaluation loop
-#define WOIT_EVPIPE 1
+#ifndef WOIT_EVPIPE  // software-pipelined evaluation loop (2: unrolled by two, no register copies)
+#define WOIT_EVPIPE 2
 #endif
 #ifndef WOIT_BPIPE
 #define WOIT_BPIPE 0
@@ -323,7 +323,53 @@ WOIT_D void eval_chunk_fast(const zfix_t* __restrict__ zf, const float* __restri
                             const float* __restrict__ opw, const CELLS cq2,
                             float* __restrict__ rad, int cst, int clen, int crot, int sh4, float ac[3],
                             float wg[3]) {
-#if WOIT_EVPIPE
+#if WOIT_EVPIPE == 2
+    // software-pipelined and unrolled by two: two operand sets alternate, so the
+    // pipeline needs no register copies (same visiting and summation order)
+    if (clen <= 0) return;
+    struct Ops {
+        float al, t, L[3], op[3];
+        float2 vd[3];
+        int si;
+    };
+    auto load = [&](int jj, Ops& o) {
+        const int fr = cst + jj;
+        o.si = sh4 + fr;
+        o.al = alp[o.si];
+        int c0;
+        eval_cell(zf[fr], R, c0, o.t);
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            o.L[ch] = rad[3 * o.si + ch];
+            o.op[ch] = opw[3 * o.si + ch];
+            o.vd[ch] = cq2.get(c0, ch);
+        }
+    };
+    auto step = [&](const Ops& o) {
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            const float A = fmaxf(fmaf(o.t, o.vd[ch].y, o.vd[ch].x), 0.0f);
+            const float vh = exp_neg(A);
+            ac[ch] += (o.L[ch] * o.al) * vh;
+            wg[ch] += o.op[ch] * vh;
+            rad[3 * o.si + ch] = vh;  // v̂ replaces radiance in place
+        }
+    };
+    auto nxt = [&](int jj) { return jj + 1 == clen ? 0 : jj + 1; };
+    Ops a, b;
+    int ja = crot;
+    load(ja, a);
+#pragma unroll 1
+    for (int j = 0; j < clen; j += 2) {
+        const int jb = nxt(ja);
+        load(jb, b);  // wrap-around prefetch past the last fragment: discarded
+        step(a);
+        if (j + 1 >= clen) break;
+        ja = nxt(jb);
+        load(ja, a);
+        step(b);
+    }
+#elif WOIT_EVPIPE
     // software-pipelined: the next fragment's operands -- and, at depth 2, its cell
     // pair -- are loaded before this fragment's v̂ stores (different fragments, so
     // no hazard; the wrap-around prefetch after the last fragment is discarded)

@@ -269,6 +269,19 @@ struct CellsCol {
     }
 };
 
+// t / n for 0 <= t < 32 and 1 <= n <= 8 (the (pixel, channel) lane split of a
+// sub-tile) by a multiply-shift: with m = ceil(256 / n), t m / 256 exceeds t / n by
+// less than 1/8, and t / n's fraction is at most 7/8, so the floor is exact.
+__constant__ uint32_t kDivMagic8[9] = {0u, 256u, 128u, 86u, 64u, 52u, 43u, 37u, 32u};
+WOIT_D int div_small(int t, int n) { return (int)(((uint32_t)t * kDivMagic8[n]) >> 8); }
+
+// kSqrt2Pow[n] / 2^(R+1) as a compile-time constant (the same literals as kSqrt2Pow)
+template <int R>
+WOIT_D constexpr double kSqrt2PowOverM(int n) {
+    return (n == 0 ? 1.0 : n == 1 ? 1.4142135623730951 : n == 2 ? 2.0 : n == 3 ? 2.8284271247461903
+            : n == 4 ? 4.0 : n == 5 ? 5.656854249492381 : 8.0) / (double)(2 << R);
+}
+
 // Haar analysis of the staircase (cell averages T[0..M)) in f64, wavelet.py:3-9
 // layout: c[2^n + k] = 2^(n/2)/M (sum left half - sum right half), c[0] = mean.
 // T is consumed.
@@ -281,7 +294,9 @@ WOIT_D void haar_analysis(double T[], double c[]) {
 #pragma unroll
         for (int k = 0; k < half; ++k) {
             const double x = T[2 * k], y = T[2 * k + 1];
-            c[half + k] = dmul(dmul(dsub(x, y), kSqrt2Pow[R - m]), 1.0 / M);
+            // (x - y) 2^((R-m)/2) / M in one rounding: 1/M is a power of two, so
+            // RN(RN(d s) / M) == RN(d (s / M)) (no underflow at these magnitudes)
+            c[half + k] = dmul(dsub(x, y), kSqrt2PowOverM<R>(R - m));
             T[k] = dadd(x, y);
         }
     }
@@ -639,7 +654,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
     int64_t pw0 = 0;
     auto composite_fast = [&](int cq0, int cnqs, int64_t cw0, float bgr) {
         if (lane >= 3 * cnqs) return;
-        const int kch = lane / cnqs, kq = lane - kch * cnqs;
+        const int kch = div_small(lane, cnqs), kq = lane - kch * cnqs;
         const int q = cq0 + kq;
         const int64_t p = cw0 + q;
         const int nc = (sm.cb[q + 1] - sm.cb[q]);
@@ -660,7 +675,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
     // this lane's opaque colour of the pending composite, from the staged copy
     auto pending_bg = [&]() -> float {
         if (!pend || lane >= 3 * pnqs || !kp.b.output) return 0.0f;
-        const int kch = lane / pnqs, kq = lane - kch * pnqs;
+        const int kch = div_small(lane, pnqs), kq = lane - kch * pnqs;
         const int si = (int)(pw0 + pq0 + kq - ((pw0 + pq0) & ~(int64_t)3));
         return sm.opq[3 * si + kch];
     };
@@ -1245,7 +1260,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
             const int t = lane;
             const int ntask = nqs * 3;
             const bool task = t < ntask;
-            const int kch = task ? t / nqs : 0, kq = task ? t - kch * nqs : 0;
+            const int kch = task ? div_small(t, nqs) : 0, kq = task ? t - kch * nqs : 0;
             double c[S];
             float rc[M];
             // Few deep pixels (>= 64 fragments each, <= 4 per sub-tile): the (pixel,

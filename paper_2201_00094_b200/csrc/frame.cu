@@ -727,7 +727,12 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
             }
             if (diffuse) df += al * vs;  // diffusion coverage (woit.h WOIT_DIFFUSION)
             if (refr && io > 1.0f) {
+#if WOIT_NRM_GLOBAL
+                const float* gn = kp.f.normal + 3 * (fa_ + fr);
+                const float nrm[3] = {gn[0], gn[1], gn[2]};
+#else
                 const float nrm[3] = {sm.normal[3 * si], sm.normal[3 * si + 1], sm.normal[3 * si + 2]};
+#endif
                 double off[2];
                 refraction_offset(kp, d, topq, sm.depth[si], nrm, io, off);
                 ro[0] += off[0];
@@ -834,7 +839,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
         // 16-fragment granule and their own window.
         {
             const bool w_ior = GEN && need_ior && kp.f.ior;
-            const bool w_nrm = GEN && refr;
+            const bool w_nrm = GEN && refr && !WOIT_NRM_GLOBAL;
             const bool w_bf = GEN && bfonly && kp.f.backface;
             int64_t b4 = (fb + 3) & ~(int64_t)3;
             b4 = b4 < (nalloc & ~(int64_t)3) ? b4 : (nalloc & ~(int64_t)3);

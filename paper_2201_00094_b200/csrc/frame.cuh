@@ -62,6 +62,9 @@ struct WT {
     static constexpr int VR = V + ((35 - V % 32) % 32);  // row stride == 3 (mod 32), >= V
 };
 
+#ifndef WOIT_NRM_GLOBAL  // refraction normals read from global memory in the evaluation (not staged)
+#define WOIT_NRM_GLOBAL 1
+#endif
 #ifndef WOIT_CHUNKLANE  // chunk descriptors computed by each chunk lane (no table)
 #define WOIT_CHUNKLANE 1
 #endif
@@ -83,7 +86,7 @@ WOIT_HD WLayout make_wlayout(uint32_t phases, int flags, bool alias_z) {
     const bool ev = phases & PH_EVAL;
     const bool need_ior = at && (flags & (WOIT_CUBE_TRANSMISSION | WOIT_REFRACTION));
     const bool need_bf = at && (flags & WOIT_CUBE_TRANSMISSION) && (flags & WOIT_CUBE_BACKFACE_ONLY);
-    const bool need_nrm = ev && (flags & WOIT_REFRACTION);
+    const bool need_nrm = !WOIT_NRM_GLOBAL && ev && (flags & WOIT_REFRACTION);
     const bool packed = (phases & PH_BUILD) && (flags & WOIT_PACKED_STORAGE);
     const uint32_t FS = G::FBW + 4;  // staging window: [fa & ~3, fb)
     WLayout L;

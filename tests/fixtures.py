@@ -56,3 +56,8 @@ def input_stream(meta, d) -> synth.SynthFrame:
 def scene_is_exact(meta) -> bool:
     """Synthetic fixtures are generated in fp32, so their f64 upcast is exact."""
     return meta["kind"] == "synth"
+
+
+def exact_names():
+    """Fixtures whose inputs are fp32-exact (synthetic), so z compares bitwise."""
+    return [n for n in names() if scene_is_exact(load(n)[0])]

@@ -430,7 +430,8 @@ WOIT_D void refraction_offset(const KParams& kp, const double d[3], double t_opq
     const double w2 = dsub(dadd(dmul(x, d[2]), dmul(s, td2)), dmul(t_opq, d[2]));
     const double* Rv = kp.p.cam_right;
     const double* U = kp.p.cam_up;
-    const double scale = dmul(kp.p.refraction_scale, ddiv((double)kp.f.width, 512.0));
+    // W / 512 == W * 2^-9 exactly (an integer times a power of two): no f64 division
+    const double scale = dmul(kp.p.refraction_scale, dmul((double)kp.f.width, 0x1p-9));
     const double ox = dmul(dadd(dadd(dmul(w0, Rv[0]), dmul(w1, Rv[1])), dmul(w2, Rv[2])), scale);
     const double oy = dmul(-dadd(dadd(dmul(w0, U[0]), dmul(w1, U[1])), dmul(w2, U[2])), scale);
     if (isfinite(ox) && isfinite(oy)) {

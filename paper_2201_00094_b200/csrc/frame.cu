@@ -1103,10 +1103,18 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
         // reduction order never depends on the tiling
 #if WOIT_CHUNKLANE
         int cq = 0, cst = 0, clen = 0, crot = 0;
-        if (lane < C) {
-            const int cb0 = sm.cb[q0];
+        const int cb0 = sm.cb[q0];
+        {   // q = the last sub-tile pixel whose first chunk is at or before l: lane j
+            // holds pixel j's first chunk (non-decreasing in j), binary search by shuffles
+            static_assert((SUBP & (SUBP - 1)) == 0 && SUBP <= 32, "SUBP: power of two");
+            const int sj = lane < nqs ? sm.cb[q0 + lane] - cb0 : 0x7fffffff;
 #pragma unroll
-            for (int j = 1; j < SUBP; ++j) cq += (j < nqs && sm.cb[q0 + j] - cb0 <= lane) ? 1 : 0;
+            for (int step = SUBP / 2; step >= 1; step >>= 1) {
+                const int v = __shfl_sync(0xffffffffu, sj, cq + step);
+                if (v <= lane) cq += step;
+            }
+        }
+        if (lane < C) {
             const int q = q0 + cq;
             const int st = (lane - (sm.cb[q] - cb0)) * CH;
             const int64_t oq = sm.offs[q];

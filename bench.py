@@ -278,7 +278,7 @@ def run_ours(args, cfg):
     # end to end through the public API: pinned host stream -> device, render, image -> host
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, W, frame, rcfg, dev, world, pg)
+        e2e = run_e2e(args, W, frame, rcfg, dev, world, pg, out)
 
     peak, peak_kind = peaks()
     if args.traffic is None:
@@ -324,7 +324,7 @@ def run_ours(args, cfg):
         pg.destroy_process_group()
 
 
-def run_e2e(args, W, frame, rcfg, dev, world, pg):
+def run_e2e(args, W, frame, rcfg, dev, world, pg, ref_image=None):
     """Same metric through the public API with host buffers: every step copies the
     step's fragment stream host->device (pinned), renders, and reads the image back.
     Uploads are double-buffered on a copy stream, so step i+1's upload overlaps step
@@ -389,12 +389,17 @@ def run_e2e(args, W, frame, rcfg, dev, world, pg):
     t1.record(stream)
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / k
+    # the image read back to the host against the device-resident run's image
+    diff = None
+    if ref_image is not None:
+        diff = float((img_host - ref_image.cpu()).abs().max()) if img_host.numel() else 0.0
     if world > 1:
         t = torch.tensor([ms], device=dev)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         ms = float(t[0])
     return {"value": frame.nfrag * world / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": k}
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": k,
+            "image_max_abs_diff_vs_device_run": diff}
 
 
 def main():

@@ -16,8 +16,12 @@
  *  - calls are asynchronous and stream-ordered; the return value reports
  *    argument validation and launch errors only (negative = error).
  *  - results are deterministic: per-pixel reductions run in an order fixed by
- *    the CSR order, the pixel id and the fragment id, so any row-band split
- *    (pixel_base/frag_base) yields bit-identical outputs.
+ *    the global pixel id (pixel_base + band-local id), the pixel's run length
+ *    and the fragment's position in its run, so any row-band split yields
+ *    bit-identical outputs as long as every band carries its pixel_base;
+ *  - a workspace `ws` carries per-launch state (the frame kernels' window-claim
+ *    counter and long-pixel list, zeroed by each call): launches that may run
+ *    concurrently (different streams or host threads) must not share one.
  *
  * Data layout (SoA, CSR by pixel — the reference's FrameFragments contract,
  * scene.py:367-392, in fp32 instead of f64):
@@ -78,7 +82,8 @@ typedef struct woit_frags {
     int64_t npix;         /* pixels in this band = len(offsets) - 1   */
     int64_t nfrag;        /* element count of the fragment arrays (>= offsets[npix]) */
     int64_t pixel_base;   /* global id of the band's first pixel (pipeline.py:321-330) */
-    int64_t frag_base;    /* global id of fragment index 0 of this band's arrays */
+    int64_t frag_base;    /* informational only (global id of fragment 0 of the band); the
+                             kernels do not read it: outputs depend on pixel_base alone */
     const int64_t* offsets;
     const float* depth;
     const float* alpha;

@@ -9,6 +9,10 @@
 //              bulk copies (cp.async.bulk + mbarrier), read once from HBM;
 //   per-pixel reductions (bounds, coefficients, accumulators) combine the
 //   chunk partials in a fixed order in fp64 -> deterministic for any tiling.
+#include <mutex>
+#include <utility>
+#include <vector>
+
 #include "frame.cuh"
 
 #ifndef WOIT_UNROLL
@@ -64,14 +68,18 @@ constexpr int kZUnroll = WOIT_ZUNROLL;  // z-loop unroll
 
 namespace woit {
 
-// Within-chunk iteration starts at a rotation that depends only on the global
-// fragment id of the chunk start: it spreads the lanes of a warp over the 32
-// smem banks for uniform run lengths and keeps the summation order independent
-// of the tiling (bit-identical results for any band split).
-WOIT_D int chunk_rotation(int64_t gstart, int len) {
-    const uint32_t g = (uint32_t)(gstart >> 5);
+// Within-chunk iteration starts at a rotation that depends only on the chunk's
+// key = gpix * run + st (global pixel id, the pixel's run length, the chunk's first
+// fragment within the pixel). For a uniform stream of L fragments per pixel the
+// key is the global id of the chunk's first fragment, so lanes spread over the
+// 32 smem banks; and as a function of (global pixel, run, chunk) only, the
+// summation order -- hence every output bit -- is independent of the tiling and
+// of how the frame is cut into bands (pixel_base is all a band needs to carry).
+WOIT_D int chunk_rotation(int64_t key, int len) {
+    const uint32_t g = (uint32_t)(key >> 5);
     return (int)(len == 8 ? (g & 7u) : g % (uint32_t)len);  // full chunks: no division
 }
+WOIT_D int64_t chunk_key(int64_t gpix, int run, int st) { return gpix * (int64_t)run + st; }
 
 
 // ---------------------------------------------------------------------------
@@ -527,9 +535,6 @@ struct WSmem {
     float* normal;
     uint8_t* bf;
     zfix_t* zfix;      // [FBW] z in fixed point, by fragment
-#if !WOIT_CHUNKLANE
-    uint32_t* chunk;   // [32]
-#endif
     float* part;       // [V][32] chunk partials (f64 [WIN][V] scratch for packed storage)
     float2* cells;     // [SUBP][M][3] (v_c, v_{c+1} - v_c): staircase at cell centres
     float* coef32;     // [WIN][V] coefficients, bulk-stored to bufs->coeffs
@@ -558,9 +563,6 @@ WOIT_D WSmem<R, GEN> wcarve(unsigned char* base, const WLayout& L) {
     s.normal = reinterpret_cast<float*>(base + L.normal);
     s.bf = reinterpret_cast<uint8_t*>(base + L.bf);
     s.zfix = reinterpret_cast<zfix_t*>(base + L.zfix);
-#if !WOIT_CHUNKLANE
-    s.chunk = reinterpret_cast<uint32_t*>(base + L.chunk);
-#endif
     s.part = reinterpret_cast<float*>(base + L.part);
     s.cells = reinterpret_cast<float2*>(base + L.cells);
     s.coef32 = reinterpret_cast<float*>(base + L.coef32);
@@ -922,7 +924,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
                 const int64_t oq = sm.offs[q0 + lane];
                 clen = (int)(sm.offs[q0 + lane + 1] - oq);
                 cst = (int)(oq - fa);
-                crot = chunk_rotation(kp.f.frag_base + fa + cst, clen);
+                crot = chunk_rotation(chunk_key(kp.f.pixel_base + p, clen, 0), clen);
             }
             if (kp.use_tma) {
                 mbar_wait(sm.bar, parity);
@@ -1101,7 +1103,6 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
         // pixels whose chunks end at or before l, and chunk i of a pixel is fragments
         // [CH i, min(CH (i+1), run)) -- a function of the run length only, so the
         // reduction order never depends on the tiling
-#if WOIT_CHUNKLANE
         int cq = 0, cst = 0, clen = 0, crot = 0;
         const int cb0 = sm.cb[q0];
         {   // q = the last sub-tile pixel whose first chunk is at or before l: lane j
@@ -1121,31 +1122,8 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
             const int run = (int)(sm.offs[q + 1] - oq);
             cst = (int)(oq - fa) + st;
             clen = run - st < CH ? run - st : CH;
-            crot = chunk_rotation(kp.f.frag_base + fa + cst, clen);
+            crot = chunk_rotation(chunk_key(kp.f.pixel_base + w0 + q, run, st), clen);
         }
-#else
-        int cq = 0, cst = 0, clen = 0, crot = 0;
-        if (lane < nqs) {
-            const int q = q0 + lane;
-            const int run = (int)(sm.offs[q + 1] - sm.offs[q]);
-            const int nc = (sm.cb[q + 1] - sm.cb[q]);
-            const int base = sm.cb[q] - sm.cb[q0];
-            const int rel = (int)(sm.offs[q] - fa);
-            for (int i = 0; i < nc; ++i) {
-                const int st = i * CH;
-                sm.chunk[base + i] = (uint32_t)lane | ((uint32_t)(rel + st) << 8) |
-                                     ((uint32_t)(run - st < CH ? run - st : CH) << 21);
-            }
-        }
-        __syncwarp();
-        if (lane < C) {
-            const uint32_t cd = sm.chunk[lane];
-            cq = (int)(cd & 255u);
-            cst = (int)((cd >> 8) & 8191u);
-            clen = (int)(cd >> 21);
-            crot = chunk_rotation(kp.f.frag_base + fa + cst, clen);
-        }
-#endif
         if (lane < nqs) {
             const int64_t p = w0 + q0 + lane;
             const bool init_empty = (ph & PH_BOUNDS) && !(ph & PH_BOUNDS_ACC);
@@ -1651,6 +1629,7 @@ __global__ void __launch_bounds__(kLongT) long_pixel_kernel(const __grid_constan
             ff_s = ff;
         }
         __syncthreads();
+        if (!(ph & (PH_BUILD | PH_EVAL | PH_COMPOSITE))) continue;  // step1 alone: bounds only
         const DepthMap m = depth_map(nf_s, ff_s, R);
         // build
         if (ph & PH_BUILD) {
@@ -1803,24 +1782,54 @@ size_t long_smem_bytes() {
     return (size_t)V * TL * 8 + (size_t)V * 8 + (size_t)V * 4;
 }
 
+// Per-(kernel, device, dynamic smem size) launch configuration, computed once: the
+// smem opt-in attribute and the occupancy query are host calls worth microseconds,
+// which showed at short frames (config 3) and in the step-wise API. Errors of these
+// calls are returned, never cleared (a pending error of an unrelated earlier launch
+// stays visible to the caller).
+struct LaunchKey {
+    const void* fn;
+    int dev, bytes;
+    bool operator==(const LaunchKey& o) const { return fn == o.fn && dev == o.dev && bytes == o.bytes; }
+};
+struct LaunchVal {
+    int sms, per_sm;
+};
+cudaError_t launch_config(const void* fn, int threads, int bytes, int& sms, int& per_sm) {
+    static std::mutex mu;
+    static std::vector<std::pair<LaunchKey, LaunchVal>> cache;
+    int dev = 0;
+    cudaError_t err = cudaGetDevice(&dev);
+    if (err != cudaSuccess) return err;
+    const LaunchKey key{fn, dev, bytes};
+    std::lock_guard<std::mutex> lock(mu);
+    for (const auto& e : cache)
+        if (e.first == key) {
+            sms = e.second.sms;
+            per_sm = e.second.per_sm;
+            return cudaSuccess;
+        }
+    if ((err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)) != cudaSuccess) return err;
+    if ((err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return err;
+    if ((err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, bytes)) != cudaSuccess) return err;
+    if (per_sm < 1) per_sm = 1;
+    cache.push_back({key, LaunchVal{sms, per_sm}});
+    return cudaSuccess;
+}
+
 template <int R, bool GEN, bool FUS, int VAR, int FL = 0>
 cudaError_t launch_tiles(const KParams& kp, cudaStream_t st) {
     using G = WT<R>;
     const uint32_t ph = (GEN && !FUS) ? kp.phases : (PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE);
     const WLayout L = make_wlayout<R>(ph, GEN ? kp.p.flags : (kp.p.flags & WOIT_NORMALIZE), !GEN && WOIT_ALIASZ);
     const int bytes = (int)(L.total * G::WPB);
-    cudaError_t err = cudaFuncSetAttribute(frame_kernel<R, GEN, FUS, VAR, FL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    if (err != cudaSuccess) return err;
     // persistent grid: as many CTAs as can be resident, each warp loops over windows
     const int64_t warps = (kp.f.npix + G::WIN - 1) / G::WIN;
     int64_t grid = (warps + G::WPB - 1) / G::WPB;
-    int dev = 0, sms = 148, per_sm = 1;
-    if (cudaGetDevice(&dev) == cudaSuccess)
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frame_kernel<R, GEN, FUS, VAR, FL>, G::WPB * 32, bytes) !=
-            cudaSuccess || per_sm < 1)
-        per_sm = 1;
-    cudaGetLastError();
+    int sms = 148, per_sm = 1;
+    cudaError_t err = launch_config(reinterpret_cast<const void*>(frame_kernel<R, GEN, FUS, VAR, FL>), G::WPB * 32,
+                                    bytes, sms, per_sm);
+    if (err != cudaSuccess) return err;
     const int64_t resident = (int64_t)sms * per_sm * WOIT_PERSIST;
     if (WOIT_PERSIST > 0) grid = grid < resident ? grid : resident;
     if (grid > 0) {
@@ -1870,9 +1879,10 @@ cudaError_t launch_rank(const KParams& kp, cudaStream_t st) {
                                    : launch_tiles<R, true, false, kVarPlain>(kp, st);
     if (err != cudaSuccess) return err;
     const size_t ls = long_smem_bytes<R>();
-    err = cudaFuncSetAttribute(long_pixel_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ls);
-    if (err != cudaSuccess) return err;
     if (kp.f.nfrag > G::FBW) {  // a pixel deeper than FBW can only exist if nfrag > FBW
+        int sms = 0, per_sm = 0;
+        err = launch_config(reinterpret_cast<const void*>(long_pixel_kernel<R>), kLongT, (int)ls, sms, per_sm);
+        if (err != cudaSuccess) return err;
         long_pixel_kernel<R><<<64, kLongT, ls, st>>>(kp);
         err = cudaGetLastError();
     }

@@ -65,12 +65,9 @@ struct WT {
 #ifndef WOIT_NRM_GLOBAL  // refraction normals read from global memory in the evaluation (not staged)
 #define WOIT_NRM_GLOBAL 1
 #endif
-#ifndef WOIT_CHUNKLANE  // chunk descriptors computed by each chunk lane (no table)
-#define WOIT_CHUNKLANE 1
-#endif
 
 struct WLayout {
-    uint32_t offs, cb, nearu, faru, lo, den, rcp, vtot, chunk;
+    uint32_t offs, cb, nearu, faru, lo, den, rcp, vtot;
     uint32_t depth, alpha, trans, rad, ior, normal, bf, zfix, part, cells, coef32, accp, pk, opq, bar, total;
 };
 
@@ -103,7 +100,6 @@ WOIT_HD WLayout make_wlayout(uint32_t phases, int flags, bool alias_z) {
     L.rcp = o;   o = align16(o + 8u * G::SUBP);
     L.vtot = o;  o = align16(o + 8u * 3 * G::SUBP);
     static_assert(8 * 6 * G::SUBP >= 4 * 3 * 32, "sink overlay too small");
-    L.chunk = o; o = align16(o + (WOIT_CHUNKLANE ? 0u : 4u * 32));
     L.depth = o; o = align16(o + 4u * FS);
     L.alpha = o; o = align16(o + (at ? 4u * FS : 0u));
     L.trans = o; o = align16(o + (at ? 12u * FS : 0u));

@@ -210,7 +210,13 @@ def _params(cfg: RenderConfig, rank: int, rays: Optional[RayGrid] = None) -> _li
 
 
 class Workspace:
-    """Device scratch for the frame kernels, grown on demand and reused."""
+    """Device scratch for the frame kernels, grown on demand and reused.
+
+    A workspace holds per-launch state (the window-claim counter and the
+    long-pixel list, include/woit.h): give each stream / host thread that may
+    launch concurrently its own. Without one, every call takes fresh scratch from
+    torch's stream-ordered caching allocator, which is safe under any concurrency.
+    """
 
     def __init__(self):
         self.buf: Optional[torch.Tensor] = None
@@ -221,7 +227,10 @@ class Workspace:
         return self.buf
 
 
-_WS = Workspace()
+def _scratch(nbytes: int, device, ws: Optional[Workspace]) -> torch.Tensor:
+    if ws is not None:
+        return ws.get(nbytes, device)
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
 
 
 def _stream() -> int:
@@ -231,8 +240,8 @@ def _stream() -> int:
 def _frame_ws(frame: FrameFragments, ws: Optional[Workspace]):
     lib = _lib.load()
     n = lib.woit_frame_workspace_bytes(frame.npix, frame.nfrag)
-    t = (ws or _WS).get(n, frame.device)
-    return ptr(t), t.numel()
+    t = _scratch(n, frame.device, ws)
+    return t, t.numel()
 
 
 def _check_frame(frame: FrameFragments, bufs: FrameBuffers) -> None:
@@ -259,7 +268,7 @@ def step1_depth_bounds(frame: FrameFragments, bufs: FrameBuffers, ws: Optional[W
     lib = _lib.load()
     f, b = frame.c_struct(), bufs.c_struct()
     w, wn = _frame_ws(frame, ws)
-    _lib.check(lib.woit_step1_depth_bounds(f, b, w, wn, _stream()), "step1_depth_bounds")
+    _lib.check(lib.woit_step1_depth_bounds(f, b, ptr(w), wn, _stream()), "step1_depth_bounds")
 
 
 def step2_build(frame: FrameFragments, bufs: FrameBuffers, cfg: RenderConfig,
@@ -269,7 +278,7 @@ def step2_build(frame: FrameFragments, bufs: FrameBuffers, cfg: RenderConfig,
     lib = _lib.load()
     f, b = frame.c_struct(), bufs.c_struct()
     w, wn = _frame_ws(frame, ws)
-    _lib.check(lib.woit_step2_build(f, _params(cfg, bufs.rank), b, w, wn, _stream()), "step2_build")
+    _lib.check(lib.woit_step2_build(f, _params(cfg, bufs.rank), b, ptr(w), wn, _stream()), "step2_build")
     if counter is not None:
         counter.record_insert(frame.nfrag, frame.nfrag * (bufs.rank + 2))
 
@@ -297,7 +306,7 @@ def step2_build_atomic(frame: FrameFragments, bufs: FrameBuffers, cfg: RenderCon
     if pix.dtype != torch.int32 or pix.numel() < frame.nfrag:
         raise ValueError("pix must be int32 with one id per fragment")
     n = lib.woit_build_atomic_workspace_bytes(frame.npix)
-    t = (ws or _WS).get(n, frame.device)
+    t = _scratch(n, frame.device, ws)
     f, b = frame.c_struct(), bufs.c_struct()
     _lib.check(lib.woit_build_atomic(f, ptr(pix), _params(cfg, bufs.rank), b, ptr(t), t.numel(), _stream()),
                "step2_build_atomic")
@@ -317,7 +326,7 @@ def step3_accumulate(rays, frame: FrameFragments, bufs: FrameBuffers, cfg: Rende
         frame = FrameFragments(**{**frame.__dict__, "pixel_base": pixel_base})
     f, b = frame.c_struct(), bufs.c_struct()
     w, wn = _frame_ws(frame, ws)
-    _lib.check(lib.woit_step3_accumulate(f, _params(cfg, bufs.rank, rays), b, w, wn, _stream()),
+    _lib.check(lib.woit_step3_accumulate(f, _params(cfg, bufs.rank, rays), b, ptr(w), wn, _stream()),
                "step3_accumulate")
     if counter is not None and frame.nfrag:
         counter.record_eval(2 * frame.nfrag, 2 * frame.nfrag * (bufs.rank + 2))
@@ -338,13 +347,11 @@ def resolve_blur(image: torch.Tensor, radius: int, ws: Optional[Workspace] = Non
     H, W = int(img.shape[0]), int(img.shape[1])
     out = torch.empty_like(img)
     n = lib.woit_blur_workspace_bytes(W, H)
-    t = (ws or _BLUR_WS).get(n, img.device)
+    t = _scratch(n, img.device, ws)
     _lib.check(lib.woit_resolve_blur(ptr(img), W, H, int(radius), ptr(out), ptr(t), t.numel(), _stream()),
                "resolve_blur")
     return out
 
-
-_BLUR_WS = Workspace()
 
 
 def _background_image(bufs_or_frame, full_opaque_image: Optional[torch.Tensor]) -> torch.Tensor:
@@ -393,7 +400,7 @@ def render_band(frame: FrameFragments, cfg: RenderConfig, rays: Optional[RayGrid
         blurred_image = resolve_blur(_background_image(frame, full_opaque_image), cfg.diffusion_radius)
     f, b = frame.c_struct(), bufs.c_struct(full_opaque_image, blurred_image)
     w, wn = _frame_ws(frame, ws)
-    _lib.check(lib.woit_render_band(f, _params(cfg, bufs.rank, rays), b, w, wn, _stream()),
+    _lib.check(lib.woit_render_band(f, _params(cfg, bufs.rank, rays), b, ptr(w), wn, _stream()),
                "render_band")
     if counter is not None:
         counter.record_insert(frame.nfrag, frame.nfrag * (cfg.rank + 2))
@@ -454,7 +461,7 @@ def render_baseline(frame: FrameFragments, cfg: RenderConfig, ws: Optional[Works
     method = _METHOD_IDS[cfg.method]
     out = torch.empty(frame.npix, 3, dtype=torch.float32, device=frame.device)
     n = lib.woit_baseline_workspace_bytes(method, frame.npix, frame.nfrag)
-    t = (ws or _WS).get(n, frame.device)
+    t = _scratch(n, frame.device, ws)
     wb = (C.c_double * 3)(*[float(x) for x in cfg.wboit_weight])
     flags = _lib.CUBE_TRANSMISSION if cfg.cube_transmission else 0
     _lib.check(lib.woit_render_baseline(frame.c_struct(), method, flags, C.cast(wb, C.c_void_p), ptr(out),

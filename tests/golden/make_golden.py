@@ -214,12 +214,26 @@ def cast_case():
     save("cast", **out)
 
 
+def deep_cases():
+    """> 160 fragments per pixel (the deep-frame kernel instance, configs 5) at the
+    other ranks config 5 sweeps: 8 and 32 coefficients (rank 4: one warp per CTA,
+    its own shared-memory layout), plus a 320-fragment rank-2 case (deeper than
+    one 256-fragment sub-tile: the long-pixel kernel)."""
+    synth_case("particles_256_r2", "particles", 8, 6, 10, 256, rank=2)
+    synth_case("particles_256_r4", "particles", 8, 6, 11, 256, rank=4)
+    synth_case("particles_192_r4", "particles", 12, 5, 12, 192, rank=4)
+    synth_case("particles_320_r2", "particles", 6, 4, 13, 320, rank=2)
+
+
 def main():
     if "--only-baselines" in sys.argv:
         baselines_case()
         return
     if "--only-cast" in sys.argv:
         cast_case()
+        return
+    if "--only-deep" in sys.argv:
+        deep_cases()
         return
     # config 1 of BASELINE.json: 64x64, the single-plane pane + 4 random layers, rank 3
     synth_case("plane4_64", "plane4", 64, 64, 1, 5, rank=3)
@@ -229,6 +243,7 @@ def main():
     synth_case("ragged_r3_linear", "ragged", 16, 12, 5, 40, rank=3, normalize=False)
     # deep pixels: the precision regime of configs 4/5
     synth_case("particles_256", "particles", 8, 6, 9, 256, rank=3)
+    deep_cases()
     synth_case("smoke_32", "smoke", 40, 24, 2, 32, rank=3)
     # reference scenes through the reference's own caster
     scene_case("wine33_refr_ca_cube", "wine-bottle", 33, 33, rank=3, refraction=True,

@@ -209,6 +209,47 @@ def test_band_split_is_bit_identical(W):
     assert torch.equal(a, b) and torch.equal(a, c)
 
 
+@pytest.mark.parametrize("workload,layers", [("ragged", 40), ("smoke", 32), ("particles", 128), ("ragged", 6)])
+def test_band_needs_only_pixel_base(W, workload, layers):
+    """A band built from host arrays (from_synth / from_numpy: pixel_base set, the
+    informational frag_base left at 0, as the reference-side binding does) renders
+    bit-identically to the same rows of the whole frame."""
+    w, hgt, r0, rows = 40, 24, 7, 11
+    whole = W.synth.generate(workload, w, hgt, seed=17, layers=layers)
+    band = W.synth.generate(workload, w, hgt, seed=17, layers=layers, row0=r0, rows=rows)
+    cfg = W.RenderConfig(rank=3, width=w, height=hgt)
+    fw = W.FrameFragments.from_synth(whole)
+    fb = W.FrameFragments.from_synth(band)
+    assert fb.frag_base == 0 and fb.pixel_base == r0 * w
+    a = W.render_band(fw, cfg, vhat=True)
+    b = W.render_band(fb, cfg, vhat=True)
+    torch.cuda.synchronize()
+    p0, p1 = r0 * w, (r0 + rows) * w
+    f0, f1 = int(whole.offsets[p0]), int(whole.offsets[p1])
+    for name in ("coeffs", "output", "accum", "accum_weight", "near"):
+        assert torch.equal(getattr(a, name)[p0:p1], getattr(b, name)), name
+    assert torch.equal(a.vhat[f0:f1], b.vhat)
+
+
+def test_concurrent_streams_without_shared_workspace(W):
+    """Launches on two streams at once, each without an explicit workspace: the
+    per-launch window counter / long list are not shared, results are exact."""
+    frames = [W.FrameFragments.synthetic("ragged", 96, 64, seed=s, layers=300) for s in (31, 32)]
+    cfg = W.RenderConfig(rank=3, width=96, height=64)
+    want = [W.render_band(f, cfg) for f in frames]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [[], []]
+    for _ in range(8):
+        for i in (0, 1):
+            with torch.cuda.stream(streams[i]):
+                outs[i].append(W.render_band(frames[i], cfg))
+    torch.cuda.synchronize()
+    for i in (0, 1):
+        for o in outs[i]:
+            assert torch.equal(o.output, want[i].output) and torch.equal(o.coeffs, want[i].coeffs)
+
+
 @pytest.mark.parametrize("layers", [6, 12, 128, 256])
 def test_tiling_is_bit_identical(W, layers):
     """Ragged runs: shallow ones (thin sub-tiles, one pixel per lane, whose extent

@@ -40,8 +40,14 @@ def gather_image(band_out: torch.Tensor, height: int, width: int, world: int, gr
     chunk = maxrows * width
     send = band_out.new_zeros(chunk, 3)
     send[: band_out.shape[0]] = band_out
-    recv = band_out.new_empty(world * chunk, 3)
-    dist.all_gather_into_tensor(recv, send, group=group)
+    if band_out.is_cuda and dist.get_backend(group) == "gloo":
+        # gloo gathers host tensors (used by the tests that run ranks on one GPU)
+        host = [torch.empty(chunk, 3, dtype=send.dtype) for _ in range(world)]
+        dist.all_gather(host, send.cpu(), group=group)
+        recv = torch.cat(host, 0).to(band_out.device)
+    else:
+        recv = band_out.new_empty(world * chunk, 3)
+        dist.all_gather_into_tensor(recv, send, group=group)
     parts = [recv[i * chunk: i * chunk + rows * width] for i, (_, rows) in enumerate(bands)]
     return torch.cat(parts, 0).reshape(height, width, 3)
 

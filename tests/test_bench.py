@@ -51,4 +51,33 @@ def test_reference_arm_line():
     line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["impl"] == "reference" and line["unit"] == "Gfrag/s" and line["value"] > 0
     assert line["metric"] == json.load(open(os.path.join(REPO, "BASELINE.json")))["metric"]
-    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
+    assert line["cpu_baseline"]["kind"] == ("reference" if bench_mod().reference_available() else "port")
+    assert line["cpu_baseline"]["numpy"] and "cpu_model" in line["cpu_baseline"]
+    # the reference arm's config is the GPU arm's, the CPU sample size separate
+    assert line["config"] == bench_mod().config_dict(bench_mod().CONFIGS[2], 1)
+    assert line["sample_rows"] == 4
+
+
+def bench_mod():
+    spec = importlib.util.spec_from_file_location("bench_t", os.path.join(REPO, "bench.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def test_gpus_relaunch_under_torchrun(bench):
+    """--gpus N outside torchrun re-launches N ranks (127.0.0.1 rendezvous)."""
+    cmd = bench.relaunch_cmd(["--gpus", "8", "--steps", "5"], 8, 29555)
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=8" in cmd and cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-3:] == ["--gpus", "8", "--steps", "5"][-3:] and cmd[-5].endswith("bench.py")
+
+
+def test_config_dicts(bench):
+    c2 = bench.config_dict(bench.CONFIGS[2], 8)
+    assert c2["height"] == 8 * 1080 and c2["fragments"] == 8 * 1920 * 1080 * 32
+    c4 = bench.config_dict(bench.CONFIGS[4], 8)
+    assert c4["height"] == 2160 and c4["fragments"] == 3840 * 2160 * 128
+    assert bench.geometry(bench.CONFIGS[4], 8) == (2160, 270)
+    assert bench.geometry(bench.CONFIGS[5], 3) == (4320, 540)

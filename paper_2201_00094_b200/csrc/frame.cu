@@ -1798,6 +1798,10 @@ struct LaunchVal {
 cudaError_t launch_config(const void* fn, int threads, int bytes, int& sms, int& per_sm) {
     static std::mutex mu;
     static std::vector<std::pair<LaunchKey, LaunchVal>> cache;
+    // the smem opt-in attribute only ever grows (per kernel and device): a launch with
+    // fewer bytes than the largest seen so far needs no new call, and lowering it would
+    // break a later launch of a cached larger size
+    static std::vector<std::pair<LaunchKey, int>> optin;
     int dev = 0;
     cudaError_t err = cudaGetDevice(&dev);
     if (err != cudaSuccess) return err;
@@ -1809,7 +1813,17 @@ cudaError_t launch_config(const void* fn, int threads, int bytes, int& sms, int&
             per_sm = e.second.per_sm;
             return cudaSuccess;
         }
-    if ((err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)) != cudaSuccess) return err;
+    int* cur = nullptr;
+    for (auto& e : optin)
+        if (e.first.fn == fn && e.first.dev == dev) cur = &e.second;
+    if (!cur || *cur < bytes) {
+        if ((err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)) != cudaSuccess)
+            return err;
+        if (cur)
+            *cur = bytes;
+        else
+            optin.push_back({LaunchKey{fn, dev, 0}, bytes});
+    }
     if ((err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return err;
     if ((err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, bytes)) != cudaSuccess) return err;
     if (per_sm < 1) per_sm = 1;

@@ -38,9 +38,6 @@
 #ifndef WOIT_EVPIPE  // software-pipelined evaluation loop (2: unrolled by two, no register copies)
 #define WOIT_EVPIPE 2
 #endif
-#ifndef WOIT_BPIPE
-#define WOIT_BPIPE 0
-#endif
 #ifndef WOIT_MINB  // launch bound: minimum resident 1-warp CTAs per SM (14: <= 144 registers; ptxas then picks 127, measured best)
 #define WOIT_MINB 14
 #endif
@@ -53,8 +50,8 @@
 #ifndef WOIT_GEN_DYN  // dynamic window claims in the general kernel
 #define WOIT_GEN_DYN 1
 #endif
-#ifndef WOIT_FFMA2
-#define WOIT_FFMA2 1
+#ifndef WOIT_BACC2  // build: paired FFMA2 updates of the red / green differences
+#define WOIT_BACC2 0
 #endif
 #ifndef WOIT_PERSIST  // resident CTAs per SM slot multiplier for the persistent grid (0: one CTA per 2 windows)
 #define WOIT_PERSIST 1
@@ -173,90 +170,74 @@ WOIT_D void store_cells(float2* cells, int kq, int kch, const TV v[M]) {
 template <int R>
 WOIT_D void build_prep(zfix_t* WOIT_ZR zf, const float* WOIT_ZR dep, const DepthMap& m,
                        const float* __restrict__ alp, float* __restrict__ trs, int fr, int si, zfix_t& zi,
-                       float a[3]) {
+                       float2& a01, float& a2) {
     zi = z_fixed_of(dep[si], m);
     zf[fr] = zi;
     const float al = alp[si];
-#if WOIT_FFMA2
-    {   // channels 0 and 1 paired (bit-identical to the scalar sequence), channel 2 scalar
-        const float2 one = make_float2(1.0f, 1.0f);
-        const float2 T01 = make_float2(trs[3 * si], trs[3 * si + 1]);
-        const float2 op01 = __fmul2_rn(make_float2(al, al), __fadd2_rn(one, make_float2(-T01.x, -T01.y)));
-        const float op2 = opacity_ch(al, trs[3 * si + 2], false);
-        trs[3 * si] = op01.x;  // the evaluation's weight 1 - t (pipeline.py:184)
-        trs[3 * si + 1] = op01.y;
-        trs[3 * si + 2] = op2;
-        const float2 y01 = __fadd2_rn(one, make_float2(-op01.x, -op01.y));
-        const float2 l01 = log_poly2(make_float2(fmaxf((float)kTransFloor, y01.x),
-                                                 fmaxf((float)kTransFloor, y01.y)));
-        a[0] = -l01.x;
-        a[1] = -l01.y;
-        a[2] = -log_poly(fmaxf((float)kTransFloor, 1.0f - op2));
-    }
-#else
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-        const float op = opacity_ch(al, trs[3 * si + ch], false);
-        trs[3 * si + ch] = op;  // the evaluation's weight 1 - t (pipeline.py:184)
-        a[ch] = -log_poly(fmaxf((float)kTransFloor, 1.0f - op));
-    }
-#endif
+    // channels 0 and 1 paired (bit-identical to the scalar sequence), channel 2 scalar
+    const float2 one = make_float2(1.0f, 1.0f);
+    const float2 T01 = make_float2(trs[3 * si], trs[3 * si + 1]);
+    const float2 op01 = __fmul2_rn(make_float2(al, al), __fadd2_rn(one, make_float2(-T01.x, -T01.y)));
+    const float op2 = opacity_ch(al, trs[3 * si + 2], false);
+    trs[3 * si] = op01.x;  // the evaluation's weight 1 - t (pipeline.py:184)
+    trs[3 * si + 1] = op01.y;
+    trs[3 * si + 2] = op2;
+    const float2 y01 = __fadd2_rn(one, make_float2(-op01.x, -op01.y));
+    const float2 l01 = log_poly2(make_float2(fmaxf((float)kTransFloor, y01.x), fmaxf((float)kTransFloor, y01.y)));
+    a01 = make_float2(-l01.x, -l01.y);
+    a2 = -log_poly(fmaxf((float)kTransFloor, 1.0f - op2));
 }
 
-// Difference-array part: a (1 - w) to D_j, a w to D_{j+1} of this lane's partials.
-template <int R>
-WOIT_D void build_accum(float* __restrict__ part, float* __restrict__ sink, int lane, zfix_t zi, const float a[3]) {
+// Difference-array part: a (1 - w) to D_j, a w to D_{j+1} of this lane's partials
+// column, j = floor(M z), w = M z - j. Rows start at cell ROW0 (PartRows): with the
+// fused render's own, tight bounds every j lies in [1, M-2] (the clamp changes
+// nothing for finite depths and keeps NaN depths inside the region); the step-wise
+// build (caller bounds, z may clip to 0 or 1 - 2^-24) keeps every row and drops D_M.
+template <int R, int ROW0>
+WOIT_D void d_update(float* __restrict__ part, int lane, zfix_t zi, float2 a01, float a2) {
     constexpr int M = 2 << R, WC = 32;
-    const int cell = (int)(zi >> (kZBits - (R + 1)));
+    int cell = (int)(zi >> (kZBits - (R + 1)));
     const float fr_ = u32_to_unit(zi << (R + 1), kZBits);  // M z - j_f
-    float* d = part + cell * 3 * WC + lane;
-    // D_{j+1} of the last cell lies past the staircase: a select into a scratch
-    // row instead of a divergent branch
-    float* d2 = cell + 1 < M ? d + 3 * WC : sink;
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) d[ch * WC] += a[ch] * (1.0f - fr_);
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) d2[ch * WC] += a[ch] * fr_;
+    const float w0 = 1.0f - fr_;
+    if (ROW0) cell = min(max(cell, 1), M - 2);
+    float* d = part + (cell - ROW0) * 3 * WC + lane;
+#if WOIT_BACC2
+    const float2 x = __ffma2_rn(a01, make_float2(w0, w0), make_float2(d[0], d[WC]));
+    d[0] = x.x;
+    d[WC] = x.y;
+#else
+    d[0] = fmaf(a01.x, w0, d[0]);
+    d[WC] = fmaf(a01.y, w0, d[WC]);
+#endif
+    d[2 * WC] = fmaf(a2, w0, d[2 * WC]);
+    if (ROW0 || cell + 1 < M) {
+        float* d2 = d + 3 * WC;
+        d2[0] = fmaf(a01.x, fr_, d2[0]);
+        d2[WC] = fmaf(a01.y, fr_, d2[WC]);
+        d2[2 * WC] = fmaf(a2, fr_, d2[2 * WC]);
+    }
 }
 
 // The chunk loops visit fragment (crot + j) mod clen at step j. (Fully unrolled
 // loops for full chunks measured 3.5% slower: code size. Software pipelining of
-// this loop -- the next fragment's prep beside this one's updates, WOIT_BPIPE --
-// measured 4% slower, and so did two fragments per step with paired fp32 ops
-// across them (3%); the evaluation loop's pipelining pays.)
-template <int R>
+// this loop -- the next fragment's prep beside this one's updates -- measured 4%
+// slower, and so did two fragments per step with paired fp32 ops across them
+// (3%); the evaluation loop's pipelining pays.)
+template <int R, int ROW0>
 WOIT_D void build_chunk_fast(zfix_t* WOIT_ZR zf, const float* WOIT_ZR dep, const DepthMap m,
                              const float* __restrict__ alp, float* __restrict__ trs, float* __restrict__ part,
-                             float* __restrict__ sink, int lane, int cst, int clen, int crot, int sh4) {
-#if WOIT_BPIPE
-    if (clen <= 0) return;
-    int jj = crot;
-    zfix_t zi;
-    float a[3];
-    build_prep<R>(zf, dep, m, alp, trs, cst + jj, sh4 + cst + jj, zi, a);
-#pragma unroll 1
-    for (int j = 0; j < clen; ++j) {
-        jj = jj + 1 == clen ? 0 : jj + 1;
-        zfix_t zn = 0;
-        float an[3] = {0.0f, 0.0f, 0.0f};
-        if (j + 1 < clen) build_prep<R>(zf, dep, m, alp, trs, cst + jj, sh4 + cst + jj, zn, an);
-        build_accum<R>(part, sink, lane, zi, a);
-        zi = zn;
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) a[ch] = an[ch];
-    }
-#else
+                             int lane, int cst, int clen, int crot, int sh4) {
     int jj = crot;
 #pragma unroll kUnroll
     for (int j = 0; j < clen; ++j) {
         const int fr = cst + jj;
         jj = jj + 1 == clen ? 0 : jj + 1;
         zfix_t zi;
-        float a[3];
-        build_prep<R>(zf, dep, m, alp, trs, fr, sh4 + fr, zi, a);
-        build_accum<R>(part, sink, lane, zi, a);
+        float2 a01;
+        float a2;
+        build_prep<R>(zf, dep, m, alp, trs, fr, sh4 + fr, zi, a01, a2);
+        d_update<R, ROW0>(part, lane, zi, a01, a2);
     }
-#endif
 }
 
 // Cell pair (v_c, v_{c+1} - v_c) for the evaluation. CellsPair reads the per-sub-tile
@@ -267,13 +248,14 @@ struct CellsPair {
     const float2* __restrict__ cq2;
     WOIT_D float2 get(int c0, int ch) const { return cq2[c0 * 3 + ch]; }
 };
-template <int M>
+template <int M, int ROW0>
 struct CellsCol {
-    const float* __restrict__ col;  // part + lane: row stride 3 x 32 floats per cell
+    const float* __restrict__ col;  // part + lane: row stride 3 x 32 floats per cell, from cell ROW0
+    WOIT_D float v(int c, int ch) const { return c < ROW0 ? 0.0f : col[(c - ROW0) * 96 + ch * 32]; }
     WOIT_D float2 get(int c0, int ch) const {
-        const float v0 = col[c0 * 96 + ch * 32];
+        const float v0 = v(c0, ch);
         const int c1 = c0 + 1 < M ? c0 + 1 : c0;
-        return make_float2(v0, col[c1 * 96 + ch * 32] - v0);
+        return make_float2(v0, v(c1, ch) - v0);
     }
 };
 
@@ -519,14 +501,12 @@ WOIT_D void empty_run(const KParams& kp, int flags, int64_t p0, int ne, int lane
 
 template <int R, bool GEN>
 struct WSmem {
-    int64_t* offs;     // [WIN+1] window CSR offsets
-    int32_t* cb;       // [WIN+1] window chunk prefix
-    uint32_t* nearu;   // [WIN]   ordered-int near / far
-    uint32_t* faru;
-    double* lo;        // [WIN]   depth map
+    int32_t* offs;     // [WIN+1] window CSR offsets, relative to the window's first fragment
+    int16_t* cb;       // [WIN+1] window chunk prefix (chunks per pixel capped at WC + 1)
+    double* lo;        // [SUBP]  depth map (general path; fast-path chunk lanes keep theirs in registers)
     double* den;
     double* rcp;
-    double* vtot;      // [WIN][3] exp(-A_total)
+    double* vtot;      // [SUBP][3] exp(-A_total)
     float* depth;      // staging [FBW+4] (granule-aligned window)
     float* alpha;
     float* trans;      // [FBW+4][3]
@@ -547,10 +527,8 @@ struct WSmem {
 template <int R, bool GEN>
 WOIT_D WSmem<R, GEN> wcarve(unsigned char* base, const WLayout& L) {
     WSmem<R, GEN> s;
-    s.offs = reinterpret_cast<int64_t*>(base + L.offs);
-    s.cb = reinterpret_cast<int32_t*>(base + L.cb);
-    s.nearu = reinterpret_cast<uint32_t*>(base + L.nearu);
-    s.faru = reinterpret_cast<uint32_t*>(base + L.faru);
+    s.offs = reinterpret_cast<int32_t*>(base + L.offs);
+    s.cb = reinterpret_cast<int16_t*>(base + L.cb);
     s.lo = reinterpret_cast<double*>(base + L.lo);
     s.den = reinterpret_cast<double*>(base + L.den);
     s.rcp = reinterpret_cast<double*>(base + L.rcp);
@@ -583,6 +561,9 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
     constexpr int VR = G::VR;  // padded row of the cell table: (pixel, channel) lanes hit distinct banks
     constexpr int M = S;       // cells
     constexpr uint32_t kFused = PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE;
+    // partials rows start at cell kRow0 (PartRows): 1 when the bounds are the fused
+    // render's own (every j in [1, M-2]), 0 for the step-wise entry points
+    constexpr int kRow0 = PartRows<R>::row0(FUS), kPRows = M - kRow0;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const uint32_t ph = (GEN && !FUS) ? kp.phases : kFused;
     // FL != 0: an instance specialised for exactly these flags (all but NORMALIZE)
@@ -747,8 +728,12 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
     flush();  // the pending composite reads this window's chunk prefix
     const int64_t w0 = win * WIN;
     const int nq = (int)((kp.f.npix - w0) < WIN ? (kp.f.npix - w0) : WIN);
-    if (lane < nq) sm.offs[lane] = off_lane;
-    if (lane == 0) sm.offs[nq] = off_last;
+    // the window's offsets relative to its first fragment (int32: a window of WIN
+    // pixels holds < 2^31 fragments, include/woit.h)
+    const int64_t wbase = __shfl_sync(0xffffffffu, off_lane, 0);
+    if (off_last - wbase > (int64_t)0x7fffffff) __trap();
+    if (lane < nq) sm.offs[lane] = (int32_t)(off_lane - wbase);
+    if (lane == 0) sm.offs[nq] = (int32_t)(off_last - wbase);
     {   // prefetch the next window's offsets (consumed one window later)
         const int64_t nw = claim();
         next_win = nw;
@@ -765,9 +750,11 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
     // any fragment-free pixel in this window? (enables the empty-run shortcut below)
     const bool any_empty = __any_sync(0xffffffffu, lane < nq && sm.offs[lane + 1] == sm.offs[lane]);
     if (lane < nq) {
-        const int64_t run = sm.offs[lane + 1] - sm.offs[lane];
-        const int64_t nc64 = (run + CH - 1) / CH;
-        my_nch = nc64 > (1 << 24) ? (1 << 24) : (int)nc64;  // long pixels never form a sub-tile
+        const int run = sm.offs[lane + 1] - sm.offs[lane];
+        const int nc = (int)(((unsigned)run + CH - 1) / CH);
+        // a pixel of more than WC chunks never forms a sub-tile (long-pixel kernel), so
+        // its count is capped at WC + 1: the window prefix fits 16 bits
+        my_nch = nc > WC + 1 ? WC + 1 : nc;
     }
     int inc = my_nch;
 #pragma unroll
@@ -775,7 +762,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
         const int y = __shfl_up_sync(0xffffffffu, inc, o);
         if (lane >= o) inc += y;
     }
-    if (lane < nq) sm.cb[lane + 1] = inc;
+    if (lane < nq) sm.cb[lane + 1] = (int16_t)inc;
     if (lane == 0) sm.cb[0] = 0;
     __syncwarp();
 
@@ -813,7 +800,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
         int q1 = q0 + cnt;
         if (kThinOK) {
             const int q = q0 + lane;
-            const int64_t run = q < nq ? sm.offs[q + 1] - sm.offs[q] : 0;
+            const int run = q < nq ? sm.offs[q + 1] - sm.offs[q] : 0;
             const unsigned b = __ballot_sync(0xffffffffu, run >= 1 && run <= CH);
             const int tc = b == 0xffffffffu ? 32 : __ffs(~b) - 1;
             if (tc > SUBP) {
@@ -822,7 +809,8 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
             }
         }
         const int nqs = q1 - q0;
-        const int64_t fa = sm.offs[q0], fb = sm.offs[q1];
+        const int ofa = sm.offs[q0];  // window-relative first fragment of the sub-tile
+        const int64_t fa = wbase + ofa, fb = wbase + sm.offs[q1];
         eg_fa = fa;
         const int C = sm.cb[q1] - sm.cb[q0];
         const int64_t a4 = fa & ~(int64_t)3, a16 = fa & ~(int64_t)15;
@@ -921,9 +909,9 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
             const int64_t p = w0 + q0 + lane;
             int cst = 0, clen = 0, crot = 0;
             if (act) {
-                const int64_t oq = sm.offs[q0 + lane];
-                clen = (int)(sm.offs[q0 + lane + 1] - oq);
-                cst = (int)(oq - fa);
+                const int oq = sm.offs[q0 + lane];
+                clen = sm.offs[q0 + lane + 1] - oq;
+                cst = oq - ofa;
                 crot = chunk_rotation(chunk_key(kp.f.pixel_base + p, clen, 0), clen);
             }
             if (kp.use_tma) {
@@ -950,7 +938,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
             float* part = sm.part;
             {
                 float4* pz = reinterpret_cast<float4*>(part);
-                for (int i = lane; i < (M * 3 * WC) / 4; i += 32) pz[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int i = lane; i < (kPRows * 3 * WC) / 4; i += 32) pz[i] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
             if (GEN && act) {
                 jj = crot;
@@ -961,11 +949,10 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
                 }
             }
             __syncwarp();
-            float* sink = reinterpret_cast<float*>(sm.lo) + lane;
             if (act) {
                 if (!GEN) {
-                    build_chunk_fast<R>(sm.zfix + (WOIT_ALIASZ ? sh4 : 0), sm.depth, m, sm.alpha, sm.trans, part, sink,
-                                        lane, cst, clen, crot, sh4);
+                    build_chunk_fast<R, kRow0>(sm.zfix + (WOIT_ALIASZ ? sh4 : 0), sm.depth, m, sm.alpha, sm.trans, part,
+                                               lane, cst, clen, crot, sh4);
                 } else {
                     jj = crot;
                     for (int j = 0; j < clen; ++j) {
@@ -983,14 +970,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
                             sm.trans[3 * si + ch] = op;
                             a[ch] = -log_poly(fmaxf((float)kTransFloor, 1.0f - op));
                         }
-                        const int cell = (int)(zi >> (kZBits - (R + 1)));
-                        const float fr_ = u32_to_unit(zi << (R + 1), kZBits);
-                        float* dd = part + cell * 3 * WC + lane;
-                        float* d2 = cell + 1 < M ? dd + 3 * WC : sink;
-#pragma unroll
-                        for (int ch = 0; ch < 3; ++ch) dd[ch * WC] += a[ch] * (1.0f - fr_);
-#pragma unroll
-                        for (int ch = 0; ch < 3; ++ch) d2[ch * WC] += a[ch] * fr_;
+                        d_update<R, kRow0>(part, lane, zi, make_float2(a[0], a[1]), a[2]);
                     }
                 }
             }
@@ -999,10 +979,10 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
             if (act) {
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) {
-                    float r = 0.0f;
+                    float r = 0.0f;  // v_c for c < kRow0 is 0
 #pragma unroll
-                    for (int k = 0; k < M; ++k) {
-                        float* a = part + k * 3 * WC + ch * WC + lane;
+                    for (int k = kRow0; k < M; ++k) {
+                        float* a = part + (k - kRow0) * 3 * WC + ch * WC + lane;
                         r += *a;
                         *a = r;
                     }
@@ -1013,7 +993,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
             float ac[3] = {0.f, 0.f, 0.f}, wg[3] = {0.f, 0.f, 0.f}, df = 0.f;
             double ro[2] = {0.0, 0.0};
             if (act) {
-                const CellsCol<M> col{part + lane};
+                const CellsCol<M, kRow0> col{part + lane};
                 if (!GEN) {
                     eval_chunk_fast<R>(sm.zfix + (WOIT_ALIASZ ? sh4 : 0), sm.alpha, sm.trans, col, sm.rad, cst, clen,
                                        crot, sh4, ac, wg);
@@ -1080,7 +1060,8 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
                     for (int ch = 0; ch < 3; ++ch) {
                         double T[M], c[S];
 #pragma unroll
-                        for (int k = 0; k < M; ++k) T[k] = (double)part[k * 3 * WC + ch * WC + lane];
+                        for (int k = 0; k < M; ++k)
+                            T[k] = k < kRow0 ? 0.0 : (double)part[(k - kRow0) * 3 * WC + ch * WC + lane];
                         haar_analysis<R>(T, c);
 #pragma unroll
                         for (int sl = 0; sl < S; ++sl) stg[(3 * sl + ch) * 33 + lane] = (float)c[sl];
@@ -1118,17 +1099,11 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
         if (lane < C) {
             const int q = q0 + cq;
             const int st = (lane - (sm.cb[q] - cb0)) * CH;
-            const int64_t oq = sm.offs[q];
-            const int run = (int)(sm.offs[q + 1] - oq);
-            cst = (int)(oq - fa) + st;
+            const int oq = sm.offs[q];
+            const int run = sm.offs[q + 1] - oq;
+            cst = oq - ofa + st;
             clen = run - st < CH ? run - st : CH;
             crot = chunk_rotation(chunk_key(kp.f.pixel_base + w0 + q, run, st), clen);
-        }
-        if (lane < nqs) {
-            const int64_t p = w0 + q0 + lane;
-            const bool init_empty = (ph & PH_BOUNDS) && !(ph & PH_BOUNDS_ACC);
-            sm.nearu[lane] = f2ord(init_empty ? INFINITY : kp.b.near[p]);
-            sm.faru[lane] = f2ord(init_empty ? -INFINITY : kp.b.far[p]);
         }
         if (kp.use_tma) {
             mbar_wait(sm.bar, parity);
@@ -1137,6 +1112,11 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
         __syncwarp();
 
         // ---- 3. bounds (step1) ------------------------------------------------------
+        // chunk min / max, then a segmented reduction over each pixel's chunk lanes
+        // (consecutive lanes) in order-preserving integers: the pixel's first chunk lane
+        // ends up with the pixel's bounds (exact, so independent of the order)
+        constexpr unsigned kAll = 0xffffffffu;
+        uint32_t mnu = f2ord(INFINITY), mxu = f2ord(-INFINITY);
         if (ph & PH_BOUNDS) {
             if (lane < C) {
                 float mn = INFINITY, mx = -INFINITY;
@@ -1156,22 +1136,55 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
                         mx = fmaxf(mx, x);
                     }
                 }
-                atomicMin(&sm.nearu[cq], f2ord(mn));
-                atomicMax(&sm.faru[cq], f2ord(mx));
+                mnu = f2ord(mn);
+                mxu = f2ord(mx);
             }
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t a = __shfl_down_sync(kAll, mnu, o), b = __shfl_down_sync(kAll, mxu, o);
+                const int k = __shfl_down_sync(kAll, cq, o);
+                if (lane + o < C && k == cq) {
+                    mnu = min(mnu, a);
+                    mxu = max(mxu, b);
+                }
+            }
+        }
+        float nf = INFINITY, ff = -INFINITY;
+        {
+            const int fc = lane < nqs ? sm.cb[q0 + lane] - cb0 : 0;  // the pixel's first chunk lane
+            const uint32_t pmn = __shfl_sync(kAll, mnu, fc & 31), pmx = __shfl_sync(kAll, mxu, fc & 31);
+            if (lane < nqs) {
+                const int64_t p = w0 + q0 + lane;
+                uint32_t n_ = f2ord(INFINITY), f_ = f2ord(-INFINITY);
+                if ((ph & PH_BOUNDS) && sm.cb[q0 + lane + 1] > fc + cb0) {
+                    n_ = pmn;
+                    f_ = pmx;
+                }
+                if (!(ph & PH_BOUNDS) || (ph & PH_BOUNDS_ACC)) {  // combined with the buffers' bounds
+                    n_ = min(n_, f2ord(kp.b.near[p]));
+                    f_ = max(f_, f2ord(kp.b.far[p]));
+                }
+                nf = ord2f(n_);
+                ff = ord2f(f_);
+                if ((ph & PH_BOUNDS) && kp.b.near) kp.b.near[p] = nf;
+                if ((ph & PH_BOUNDS) && kp.b.far) kp.b.far[p] = ff;
+                if (GEN) {
+                    const DepthMap m = depth_map(nf, ff, R);
+                    sm.lo[lane] = m.lo;
+                    sm.den[lane] = m.den;
+                    sm.rcp[lane] = m.rs;  // fixed-point z scale (z_fixed_of)
+                }
+            }
+        }
+        // fast path: every chunk lane derives its pixel's depth map itself (the same
+        // warp instructions as the pixel lanes computing it, no shared-memory round trip)
+        DepthMap mq{0.0, 0.0, 0.0, 0.0};
+        if (!GEN) {
+            const float cnf = __shfl_sync(kAll, nf, cq), cff = __shfl_sync(kAll, ff, cq);
+            if (lane < C) mq = depth_map(cnf, cff, R);
+        } else {
             __syncwarp();
         }
-        if (lane < nqs) {
-            const float nf = ord2f(sm.nearu[lane]), ff = ord2f(sm.faru[lane]);
-            const int64_t p = w0 + q0 + lane;
-            if ((ph & PH_BOUNDS) && kp.b.near) kp.b.near[p] = nf;
-            if ((ph & PH_BOUNDS) && kp.b.far) kp.b.far[p] = ff;
-            const DepthMap m = depth_map(nf, ff, R);
-            sm.lo[lane] = m.lo;
-            sm.den[lane] = m.den;
-            sm.rcp[lane] = m.rs;  // fixed-point z scale (z_fixed_of)
-        }
-        __syncwarp();
 
         // ---- 4. z (fixed point) and build (step2): chunk partials -> part[v][lane] ----
         float* part = sm.part;
@@ -1197,20 +1210,14 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
         // prefix sum of D. The reference's coefficients are the Haar analysis of v
         // (phase 5) -- its closed form (wavelet.py:272-287) up to rounding.
         if (ph & PH_BUILD) {
-            // this chunk's depth map, read before the sink below reuses its bytes
-            DepthMap mq{0.0, 0.0, 0.0, 0.0};
-            if (!GEN && lane < C) mq = DepthMap{sm.lo[cq], sm.den[cq], 0.0, sm.rcp[cq]};
-            {   // zero the partials [M][3][32] cooperatively, 16 B per store
+            {   // zero the partials [kPRows][3][32] cooperatively, 16 B per store
                 float4* pz = reinterpret_cast<float4*>(part);
-                for (int i = lane; i < (M * 3 * WC) / 4; i += 32) pz[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int i = lane; i < (kPRows * 3 * WC) / 4; i += 32) pz[i] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
             __syncwarp();
-            // scratch [3][32] for the dropped D_M terms: the depth maps and vtot
-            // (contiguous, >= 384 B) are dead until phase 5 / the next sub-tile
-            float* sink = reinterpret_cast<float*>(sm.lo) + lane;
             if (!GEN && lane < C) {
-                build_chunk_fast<R>(sm.zfix + (WOIT_ALIASZ ? sh4 : 0), sm.depth, mq, sm.alpha, sm.trans, part, sink,
-                                    lane, cst, clen, crot, sh4);
+                build_chunk_fast<R, kRow0>(sm.zfix + (WOIT_ALIASZ ? sh4 : 0), sm.depth, mq, sm.alpha, sm.trans, part,
+                                           lane, cst, clen, crot, sh4);
             } else if (lane < C) {
                 int jj = crot;
 #pragma unroll kUnroll
@@ -1229,14 +1236,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
                         sm.trans[3 * si + ch] = op;  // the evaluation's weight 1 - t (pipeline.py:184)
                         a[ch] = -log_poly(fmaxf((float)kTransFloor, 1.0f - op));
                     }
-                    const int cell = (int)(zi >> (kZBits - (R + 1)));
-                    const float fr_ = u32_to_unit(zi << (R + 1), kZBits);  // M z - j_f
-                    float* d = part + cell * 3 * WC + lane;
-                    float* d2 = cell + 1 < M ? d + 3 * WC : sink;
-#pragma unroll
-                    for (int ch = 0; ch < 3; ++ch) d[ch * WC] += a[ch] * (1.0f - fr_);
-#pragma unroll
-                    for (int ch = 0; ch < 3; ++ch) d2[ch * WC] += a[ch] * fr_;
+                    d_update<R, kRow0>(part, lane, zi, make_float2(a[0], a[1]), a[2]);
                 }
             }
             __syncwarp();
@@ -1289,8 +1289,9 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
                                 if (g >= 0 && g < ng) {
 #pragma unroll
                                     for (int j = 0; j < KB; ++j) {
-                                        const float4 p4 =
-                                            *reinterpret_cast<const float4*>(pv + (blk + j * B) * 3 * WC + 4 * g);
+                                        if (blk + j * B < kRow0) continue;  // D_0 (no row): 0
+                                        const float4 p4 = *reinterpret_cast<const float4*>(
+                                            pv + (blk + j * B - kRow0) * 3 * WC + 4 * g);
                                         rs[r][j] += p4.x;
                                         rs[r][j] += p4.y;
                                         rs[r][j] += p4.z;
@@ -1301,10 +1302,12 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
                         } else {
 #pragma unroll
                             for (int j = 0; j < KB; ++j) {
-                                const float* pk = pv + (blk + j * B) * 3 * WC;
                                 float x = 0.0f;
+                                if (blk + j * B >= kRow0) {
+                                    const float* pk = pv + (blk + j * B - kRow0) * 3 * WC;
 #pragma unroll 1
-                                for (int i = 0; i < nc; ++i) x += pk[i];
+                                    for (int i = 0; i < nc; ++i) x += pk[i];
+                                }
                                 rs[r][j] = x;
                             }
                         }
@@ -1350,8 +1353,8 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
 #pragma unroll 1
                     for (int i = 0; i < nc; i += 4) {
 #pragma unroll
-                        for (int k = 0; k < M; ++k) {
-                            const float4 p4 = *reinterpret_cast<const float4*>(pv + k * 3 * WC + i);
+                        for (int k = kRow0; k < M; ++k) {  // D_c for c < kRow0 is 0
+                            const float4 p4 = *reinterpret_cast<const float4*>(pv + (k - kRow0) * 3 * WC + i);
                             rc[k] += p4.x;
                             rc[k] += p4.y;
                             rc[k] += p4.z;
@@ -1362,7 +1365,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
 #pragma unroll 1
                     for (int i = 0; i < nc; ++i) {
 #pragma unroll
-                        for (int k = 0; k < M; ++k) rc[k] += pv[k * 3 * WC + i];
+                        for (int k = kRow0; k < M; ++k) rc[k] += pv[(k - kRow0) * 3 * WC + i];
                     }
                 }
                 // cell averages v_c = D_0 + ... + D_c, all terms >= 0
@@ -1482,8 +1485,10 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
                     sm.accp[ch * WC + lane] = ac[ch];
                     sm.accp[(3 + ch) * WC + lane] = wg[ch];
                 }
-                sm.accp[6 * WC + lane] = (float)ro[0];
-                sm.accp[7 * WC + lane] = (float)ro[1];
+                if (GEN) {  // the fast path's accumulators are ac / wg only (its v_tot follows them)
+                    sm.accp[6 * WC + lane] = (float)ro[0];
+                    sm.accp[7 * WC + lane] = (float)ro[1];
+                }
                 if (GEN) sm.accp[8 * WC + lane] = df;
             }
             fence_proxy_async();  // v̂ in smem becomes visible to the bulk store

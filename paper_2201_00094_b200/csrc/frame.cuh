@@ -67,15 +67,27 @@ struct WT {
 #endif
 
 struct WLayout {
-    uint32_t offs, cb, nearu, faru, lo, den, rcp, vtot;
+    uint32_t offs, cb, lo, den, rcp, vtot;
     uint32_t depth, alpha, trans, rad, ior, normal, bf, zfix, part, cells, coef32, accp, pk, opq, bar, total;
 };
 
 WOIT_HD uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
 
-// shared-memory slice of one warp (bytes); the CTA holds WPB slices. alias_z: the
-// fixed-point z overwrites the staged depth in place (fast path: the build computes
-// z and nothing reads the depth afterwards), saving the separate [FBW] array.
+// Rows of the chunk partials (per-cell differences D_c). For R >= 1 the padded depth
+// map (eval_bounds, pipeline.py:110-128) puts every fragment's z strictly inside
+// [1/M, 1 - 1/M), so j_f = floor(M z) lies in [1, M-2]: D_0 and D_M are never touched
+// and only cells 1..M-1 get a row (row c-1); v_0 = 0. Rank 0 keeps all M rows.
+// (The step-wise entry points take the caller's bounds, so they keep every row.)
+template <int R>
+struct PartRows {
+    WOIT_HD static constexpr int row0(bool tight) { return tight && R >= 1 ? 1 : 0; }  // first cell with a row
+    WOIT_HD static constexpr int n(bool tight) { return (2 << R) - row0(tight); }
+};
+
+// shared-memory slice of one warp (bytes); the CTA holds WPB slices. alias_z (the fast
+// path): the fixed-point z overwrites the staged depth in place (the build computes z
+// and nothing reads the depth afterwards), every chunk lane derives its own depth map
+// (no per-pixel map arrays), and exp(-A_total) lives in the reused partials region.
 template <int R>
 WOIT_HD WLayout make_wlayout(uint32_t phases, int flags, bool alias_z) {
     using G = WT<R>;
@@ -88,18 +100,16 @@ WOIT_HD WLayout make_wlayout(uint32_t phases, int flags, bool alias_z) {
     const uint32_t FS = G::FBW + 4;  // staging window: [fa & ~3, fb)
     WLayout L;
     uint32_t o = 0;
-    L.offs = o;  o = align16(o + 8u * (G::WIN + 1));
-    L.cb = o;    o = align16(o + 4u * (G::WIN + 1));  // chunk prefix (chunks of q = cb[q+1] - cb[q])
-    // per sub-tile pixel (<= SUBP)
-    L.nearu = o; o = align16(o + 4u * G::SUBP);
-    L.faru = o;  o = align16(o + 4u * G::SUBP);
-    // depth maps and exp(-A_total) [SUBP][3]; during the build these contiguous
-    // bytes (>= 384) are the [3][32] float sink of the dropped D_M terms
-    L.lo = o;    o = align16(o + 8u * G::SUBP);
-    L.den = o;   o = align16(o + 8u * G::SUBP);
-    L.rcp = o;   o = align16(o + 8u * G::SUBP);
-    L.vtot = o;  o = align16(o + 8u * 3 * G::SUBP);
-    static_assert(8 * 6 * G::SUBP >= 4 * 3 * 32, "sink overlay too small");
+    L.offs = o;  o = align16(o + 4u * (G::WIN + 1));  // int32, relative to the window's first fragment
+    L.cb = o;    o = align16(o + 2u * (G::WIN + 1));  // int16 chunk prefix (chunks of q = cb[q+1] - cb[q])
+    // per sub-tile pixel (<= SUBP): depth maps and exp(-A_total) [SUBP][3] (general path)
+    L.lo = L.den = L.rcp = L.vtot = o;
+    if (!alias_z) {
+        L.lo = o;    o = align16(o + 8u * G::SUBP);
+        L.den = o;   o = align16(o + 8u * G::SUBP);
+        L.rcp = o;   o = align16(o + 8u * G::SUBP);
+        L.vtot = o;  o = align16(o + 8u * 3 * G::SUBP);
+    }
     L.depth = o; o = align16(o + 4u * FS);
     L.alpha = o; o = align16(o + (at ? 4u * FS : 0u));
     L.trans = o; o = align16(o + (at ? 12u * FS : 0u));
@@ -109,16 +119,19 @@ WOIT_HD WLayout make_wlayout(uint32_t phases, int flags, bool alias_z) {
     L.bf = o;    o = align16(o + (need_bf ? (uint32_t)G::FBW + 32u : 0u));
     L.zfix = alias_z ? L.depth : o;
     o = align16(o + (at && !alias_z ? 4u * G::FBW : 0u));
-    // one region, reused: chunk partials [M][3][32] (per-cell differences D) during the
-    // build, then the sub-tile's coefficients [SUBP][V], cell staircase [SUBP][VR]
-    // and chunk accumulators [9][32]
-    const uint32_t part_b = (phases & PH_BUILD) ? 4u * G::V * 32 : 0u;
-    const uint32_t CR = 3u * G::S + ((3u + 16u * 64u - 3u * G::S) % 16u);  // frame.cu CellRow
-    const uint32_t after_b = align16(4u * G::SUBP * G::V) + align16(8u * G::SUBP * CR) + (ev ? 4u * 9 * 32 : 0u);
+    // one region, reused: chunk partials [rows][3][32] (per-cell differences D) during
+    // the build, then the sub-tile's coefficients [SUBP][V], cell staircase (frame.cu
+    // CellTab), chunk accumulators [6 or 9][32] and, on the fast path, exp(-A_total)
+    const bool tight = phases == (PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE);  // the fused render's own bounds
+    const uint32_t part_b = (phases & PH_BUILD) ? 4u * 3 * 32 * PartRows<R>::n(tight) : 0u;
+    const uint32_t cells_b = (uint32_t)G::SUBP * (G::S + 1) * 24u;  // frame.cu CellTab
+    const uint32_t acc_b = ev ? 4u * (alias_z ? 6 : 9) * 32 : 0u;
+    const uint32_t after_b = align16(4u * G::SUBP * G::V) + align16(cells_b) + acc_b + (alias_z ? 8u * 3 * G::SUBP : 0u);
     L.part = o;  o = align16(o + (part_b > after_b ? part_b : after_b));
     L.coef32 = L.part;
     L.cells = L.part + align16(4u * G::SUBP * G::V);
-    L.accp = L.cells + align16(8u * G::SUBP * CR);
+    L.accp = L.cells + align16(cells_b);
+    if (alias_z) L.vtot = L.accp + acc_b;
     L.pk = o;    o = align16(o + (packed ? 8u * G::WIN * G::V : 0u));
     L.opq = o;   o = align16(o + 12u * (G::SUBP + 4));  // [pa & ~3, pb rounded up to 4)
     L.bar = o;   o = align16(o + 16u);

@@ -498,7 +498,7 @@ struct WSmem {
     double* lo;        // [SUBP]  depth map (general path; fast-path chunk lanes keep theirs in registers)
     double* den;
     double* rcp;
-    double* vtot;      // [SUBP][3] exp(-A_total)
+    float* vtot;       // [SUBP][3] exp(-A_total) (an fp32 expf result, so fp32 holds it exactly)
     float* depth;      // staging [FBW+4] (granule-aligned window)
     float* alpha;
     float* trans;      // [FBW+4][3]
@@ -524,7 +524,7 @@ WOIT_D WSmem<R, GEN> wcarve(unsigned char* base, const WLayout& L) {
     s.lo = reinterpret_cast<double*>(base + L.lo);
     s.den = reinterpret_cast<double*>(base + L.den);
     s.rcp = reinterpret_cast<double*>(base + L.rcp);
-    s.vtot = reinterpret_cast<double*>(base + L.vtot);
+    s.vtot = reinterpret_cast<float*>(base + L.vtot);
     s.depth = reinterpret_cast<float*>(base + L.depth);
     s.alpha = reinterpret_cast<float*>(base + L.alpha);
     s.trans = reinterpret_cast<float*>(base + L.trans);
@@ -550,7 +550,7 @@ template <int R, bool GEN, bool FUS, int VAR, int FL>
 __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R>::WPB) frame_kernel(const __grid_constant__ KParams kp) {
     using G = WT<R>;
     constexpr int S = G::S, V = G::V, CH = G::CH, WC = 32, FBW = G::FBW, WIN = G::WIN, SUBP = G::SUBP;
-    constexpr int VR = G::VR;  // padded row of the cell table: (pixel, channel) lanes hit distinct banks
+    constexpr int AR = WC + 1;  // chunk-accumulator row stride: the (pixel, channel) combine lanes hit distinct banks
     constexpr int M = S;       // cells
     constexpr uint32_t kFused = PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE;
     // partials rows start at cell kRow0 (PartRows): 1 when the bounds are the fused
@@ -636,12 +636,12 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
         const int cbq = sm.cb[q] - sm.cb[cq0];
         double acc = 0.0, wgt = 0.0;
         for (int i = 0; i < nc; ++i) {
-            acc += (double)sm.accp[kch * WC + cbq + i];
-            wgt += (double)sm.accp[(3 + kch) * WC + cbq + i];
+            acc += (double)sm.accp[kch * AR + cbq + i];
+            wgt += (double)sm.accp[(3 + kch) * AR + cbq + i];
         }
         if (kp.b.accum) kp.b.accum[p * 3 + kch] = (float)acc;
         if (kp.b.weight) kp.b.weight[p * 3 + kch] = (float)wgt;
-        if (kp.b.output) kp.b.output[p * 3 + kch] = composite_fast_ch(flags, acc, wgt, (double)bgr, sm.vtot[kq * 3 + kch]);
+        if (kp.b.output) kp.b.output[p * 3 + kch] = composite_fast_ch(flags, acc, wgt, (double)bgr, (double)sm.vtot[kq * 3 + kch]);
         if (kch == 0 && kp.b.refraction_offset) {
             kp.b.refraction_offset[p * 2] = 0.0f;
             kp.b.refraction_offset[p * 2 + 1] = 0.0f;
@@ -1114,9 +1114,11 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
                 float mn = INFINITY, mx = -INFINITY;
                 if (clen == CH && ((sh4 + cst) & 3) == 0) {
                     // min / max do not depend on the order: two 16-B loads per full chunk,
-                    // the halves swapped on odd lanes to spread the banks
+                    // the halves swapped on lanes 4..7 of each quarter warp, so its eight
+                    // 16-B accesses hit distinct banks
                     const float4* d4 = reinterpret_cast<const float4*>(sm.depth + sh4 + cst);
-                    const float4 u = d4[lane & 1], w = d4[(lane & 1) ^ 1];
+                    const int h = (lane >> 2) & 1;
+                    const float4 u = d4[h], w = d4[h ^ 1];
                     mn = fminf(fminf(fminf(u.x, u.y), fminf(u.z, u.w)), fminf(fminf(w.x, w.y), fminf(w.z, w.w)));
                     mx = fmaxf(fmaxf(fmaxf(u.x, u.y), fmaxf(u.z, u.w)), fmaxf(fmaxf(w.x, w.y), fmaxf(w.z, w.w)));
                 } else {
@@ -1369,7 +1371,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
             if (task) {
                 const int q = q0 + kq;
                 if (do_eval) store_cells<M>(sm.cells, kq, kch, rc);
-                if (need_coef) sm.vtot[kq * 3 + kch] = (double)expf(-rc[M - 1]);  // A(z -> 1) = v_{M-1}
+                if (need_coef) sm.vtot[kq * 3 + kch] = expf(-rc[M - 1]);  // A(z -> 1) = v_{M-1}
                 // coefficients: Haar analysis of v in f64 (wavelet.py:3-9 layout):
                 // c[2^n + k] = 2^(n/2)/M (sum left half - sum right half), c[0] = mean
                 double T[M];
@@ -1414,7 +1416,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
                         double at = c[0];
 #pragma unroll
                         for (int n = 0; n <= R; ++n) at = dsub(at, dmul(kSqrt2Pow[n], c[(2 << n) - 1]));
-                        sm.vtot[kq * 3 + kch] = (double)expf(-(float)fmax(at, 0.0));
+                        sm.vtot[kq * 3 + kch] = expf(-(float)fmax(at, 0.0));
                     }
                     if (do_eval) {
                         double cell[S];
@@ -1433,7 +1435,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
                 double at = c[0];
 #pragma unroll
                 for (int n = 0; n <= R; ++n) at = dsub(at, dmul(kSqrt2Pow[n], c[(2 << n) - 1]));
-                sm.vtot[kq * 3 + kch] = (double)expf(-(float)fmax(at, 0.0));
+                sm.vtot[kq * 3 + kch] = expf(-(float)fmax(at, 0.0));
                 double cell[S];
                 haar_cells<R>(c, cell);
                 store_cells<M>(sm.cells, kq, kch, cell);
@@ -1474,14 +1476,14 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
                 }
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) {
-                    sm.accp[ch * WC + lane] = ac[ch];
-                    sm.accp[(3 + ch) * WC + lane] = wg[ch];
+                    sm.accp[ch * AR + lane] = ac[ch];
+                    sm.accp[(3 + ch) * AR + lane] = wg[ch];
                 }
                 if (GEN) {  // the fast path's accumulators are ac / wg only (its v_tot follows them)
-                    sm.accp[6 * WC + lane] = (float)ro[0];
-                    sm.accp[7 * WC + lane] = (float)ro[1];
+                    sm.accp[6 * AR + lane] = (float)ro[0];
+                    sm.accp[7 * AR + lane] = (float)ro[1];
                 }
-                if (GEN) sm.accp[8 * WC + lane] = df;
+                if (GEN) sm.accp[8 * AR + lane] = df;
             }
             fence_proxy_async();  // v̂ in smem becomes visible to the bulk store
             __syncwarp();
@@ -1537,13 +1539,13 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
                 const int cbq = sm.cb[q] - sm.cb[q0];
                 for (int i = 0; i < nc; ++i) {
                     const int cc = cbq + i;
-                    acc += (double)sm.accp[kch * WC + cc];
-                    wgt += (double)sm.accp[(3 + kch) * WC + cc];
+                    acc += (double)sm.accp[kch * AR + cc];
+                    wgt += (double)sm.accp[(3 + kch) * AR + cc];
                     if (refr) {
-                        ro0 += (double)sm.accp[6 * WC + cc];
-                        ro1 += (double)sm.accp[7 * WC + cc];
+                        ro0 += (double)sm.accp[6 * AR + cc];
+                        ro1 += (double)sm.accp[7 * AR + cc];
                     }
-                    if (diffuse) dsum += (double)sm.accp[8 * WC + cc];
+                    if (diffuse) dsum += (double)sm.accp[8 * AR + cc];
                 }
                 if (diffuse) dp = dadd(dp, ddiv(dsum, 3.0));
                 if (kp.b.accum) kp.b.accum[p * 3 + kch] = (float)acc;
@@ -1557,7 +1559,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
                 }
             }
             if ((ph & PH_COMPOSITE) && kp.b.output)
-                kp.b.output[p * 3 + kch] = composite_channel(kp, flags, p, kch, acc, wgt, ro0, ro1, sm.vtot[kq * 3 + kch], dp);
+                kp.b.output[p * 3 + kch] = composite_channel(kp, flags, p, kch, acc, wgt, ro0, ro1, (double)sm.vtot[kq * 3 + kch], dp);
         }
         fence_proxy_async();
         __syncwarp();

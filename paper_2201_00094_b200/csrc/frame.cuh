@@ -108,7 +108,7 @@ WOIT_HD WLayout make_wlayout(uint32_t phases, int flags, bool alias_z) {
         L.lo = o;    o = align16(o + 8u * G::SUBP);
         L.den = o;   o = align16(o + 8u * G::SUBP);
         L.rcp = o;   o = align16(o + 8u * G::SUBP);
-        L.vtot = o;  o = align16(o + 8u * 3 * G::SUBP);
+        L.vtot = o;  o = align16(o + 4u * 3 * G::SUBP);
     }
     L.depth = o; o = align16(o + 4u * FS);
     L.alpha = o; o = align16(o + (at ? 4u * FS : 0u));
@@ -125,8 +125,8 @@ WOIT_HD WLayout make_wlayout(uint32_t phases, int flags, bool alias_z) {
     const bool tight = phases == (PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE);  // the fused render's own bounds
     const uint32_t part_b = (phases & PH_BUILD) ? 4u * 3 * 32 * PartRows<R>::n(tight) : 0u;
     const uint32_t cells_b = (uint32_t)G::SUBP * (G::S + 1) * 24u;  // frame.cu CellTab
-    const uint32_t acc_b = ev ? 4u * (alias_z ? 6 : 9) * 32 : 0u;
-    const uint32_t after_b = align16(4u * G::SUBP * G::V) + align16(cells_b) + acc_b + (alias_z ? 8u * 3 * G::SUBP : 0u);
+    const uint32_t acc_b = ev ? align16(4u * (alias_z ? 6 : 9) * 33) : 0u;  // rows of 33 (frame.cu AR)
+    const uint32_t after_b = align16(4u * G::SUBP * G::V) + align16(cells_b) + acc_b + (alias_z ? 4u * 3 * G::SUBP : 0u);
     L.part = o;  o = align16(o + (part_b > after_b ? part_b : after_b));
     L.coef32 = L.part;
     L.cells = L.part + align16(4u * G::SUBP * G::V);

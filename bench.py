@@ -70,11 +70,12 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def algorithmic_bytes(npix: int, nfrag: int, rank: int) -> int:
+def algorithmic_bytes(npix: int, nfrag: int, rank: int, packed: bool = False) -> int:
     """44 B/fragment (depth, alpha, T, L in; v̂ out) +
-    (32 + 12 S) B/pixel (offsets, opaque RGB in; coefficients, image out)."""
+    (32 + 12 S) B/pixel (offsets, opaque RGB in; coefficients, image out); with packed
+    storage the coefficients leave as S E5B9G9R9 words: (32 + 4 S) B/pixel."""
     S = 1 << (rank + 1)
-    return nfrag * 44 + npix * (32 + 12 * S)
+    return nfrag * 44 + npix * (32 + (4 if packed else 12) * S)
 
 
 def scaled(cfg: dict, tiny: bool) -> dict:
@@ -346,25 +347,30 @@ class Comm:
 class Renderer:
     """One band's device buffers and its woit_render_band launch (the C ABI)."""
 
-    def __init__(self, W, lib, frame, rank_n: int, height: int):
+    def __init__(self, W, lib, frame, rank_n: int, height: int, packed: bool = False):
         import torch
 
         self.lib, self.frame = lib, frame
         P, n = frame.npix, frame.nfrag
         S = 1 << (rank_n + 1)
         dev = frame.device
-        self.coeffs = torch.empty(P, S, 3, dtype=torch.float32, device=dev)
+        # packed storage: the coefficients leave only as E5B9G9R9 words (4 S B/px)
+        self.coeffs = None if packed else torch.empty(P, S, 3, dtype=torch.float32, device=dev)
+        self.words = torch.empty(P, S, dtype=torch.int32, device=dev) if packed else None
         self.vhat = torch.empty(n, 3, dtype=torch.float32, device=dev)
         self.out = torch.empty(P, 3, dtype=torch.float32, device=dev)
         self.wsn = lib.woit_frame_workspace_bytes(P, n)
         self.ws = torch.empty(self.wsn, dtype=torch.uint8, device=dev)
         self.fs = frame.c_struct()
-        self.ps = W.pipeline._params(W.RenderConfig(rank=rank_n, width=frame.width, height=height), rank_n)
+        self.ps = W.pipeline._params(W.RenderConfig(rank=rank_n, width=frame.width, height=height,
+                                                    packed_storage=packed), rank_n)
         from paper_2201_00094_b200 import _lib
 
         self._lib = _lib
         self.bs = _lib.Bufs()
-        self.bs.coeffs, self.bs.vhat, self.bs.output = self.coeffs.data_ptr(), self.vhat.data_ptr(), self.out.data_ptr()
+        self.bs.coeffs = self.coeffs.data_ptr() if self.coeffs is not None else None
+        self.bs.coeff_words = self.words.data_ptr() if self.words is not None else None
+        self.bs.vhat, self.bs.output = self.vhat.data_ptr(), self.out.data_ptr()
 
     def launch(self, stream):
         self._lib.check(self.lib.woit_render_band(self.fs, self.ps, self.bs, self.ws.data_ptr(), self.wsn,
@@ -485,7 +491,7 @@ def run_ours(args, cfg):
     frame = W.FrameFragments.synthetic(cfg["workload"], Wd, frame_h, seed=cfg["seed"], layers=cfg["layers"],
                                        row0=H1 * rank, rows=H1, device=dev)
     lib = _lib.load()
-    r = Renderer(W, lib, frame, cfg["rank"], frame_h)
+    r = Renderer(W, lib, frame, cfg["rank"], frame_h, packed=args.packed)
     P, n = frame.npix, frame.nfrag
     image = torch.empty(P * world, 3, dtype=torch.float32, device=dev) if world > 1 else r.out
     stream = torch.cuda.current_stream(dev)
@@ -500,8 +506,8 @@ def run_ours(args, cfg):
     # end to end through the public API: pinned host stream -> device, render, image -> host
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, W, frame, W.RenderConfig(rank=cfg["rank"], width=Wd, height=frame_h), dev, world, comm,
-                      r.out)
+        e2e = run_e2e(args, W, frame, W.RenderConfig(rank=cfg["rank"], width=Wd, height=frame_h,
+                                                     packed_storage=args.packed), dev, world, comm, r.out)
     del r, image
     torch.cuda.empty_cache()
     c4 = None
@@ -509,14 +515,14 @@ def run_ours(args, cfg):
         c4 = strong_config4(args, W, lib, comm, rank, world, dev, stream)
 
     peak, peak_kind = peaks()
-    if args.traffic is None:
+    if args.traffic is None and not args.packed:
         try:
             with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
                 tj = json.load(f)
             args.traffic = tj.get(f"config{args.config}_rank{cfg['rank']}", tj.get(f"config{args.config}"))
         except Exception:
             args.traffic = None
-    alg = algorithmic_bytes(P, n, cfg["rank"])
+    alg = algorithmic_bytes(P, n, cfg["rank"], args.packed)
     achieved = alg / (kern_ms * 1e-3) / 1e9
     clocks = clk.summary()
     if rank != 0:
@@ -643,6 +649,8 @@ def main(argv=None):
     ap.add_argument("--backend", choices=("nccl", "gloo"), default="nccl",
                     help="process-group backend (gloo: tests running ranks on one GPU)")
     ap.add_argument("--tiny", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--packed", action="store_true",
+                    help="E5B9G9R9 packed coefficient storage (4 S B/px words instead of fp32 coefficients)")
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per launch from an ncu --set full capture (profiles/)")
     args = ap.parse_args(argv)
@@ -656,6 +664,8 @@ def main(argv=None):
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3  # timing rule: >= 3 warm-up steps
     cfg = scaled(dict(CONFIGS[args.config]), args.tiny)
+    if args.packed:
+        cfg["name"] += " [packed E5B9G9R9 storage: coefficients as 4 S B/px words]"
     if args.rank is not None:
         if not 0 <= args.rank <= 6:
             raise SystemExit("--rank must be in 0..6")

@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define WOIT_ABI_VERSION 2
+#define WOIT_ABI_VERSION 3
 
 /* status codes */
 #define WOIT_OK 0
@@ -124,6 +124,9 @@ typedef struct woit_bufs {
     float* diffusion;          /* [npix] coverage D_p (WOIT_DIFFUSION); NULL: not written */
     const float* blurred_image; /* WOIT_DIFFUSION: woit_resolve_blur of the background image,
                                    same extent/indexing as the image bg is read from */
+    uint32_t* coeff_words;     /* WOIT_PACKED_STORAGE: [npix][S] E5B9G9R9 words (packing.py:46-77),
+                                  word s = pack(|coefficients of slot s|), the paper's 4 S B/px
+                                  storage; NULL: not written (ABI 3) */
 } woit_bufs_t;
 
 /* ---- version / errors ---------------------------------------------------- */

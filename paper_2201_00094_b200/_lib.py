@@ -14,7 +14,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # WOIT_LIB selects an alternative build (tuning variants, tools/variants.py)
 LIB_PATH = os.environ.get("WOIT_LIB") or os.path.join(_HERE, "libwoit.so")
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 OK = 0
 EINVAL = -1
@@ -61,7 +61,7 @@ class Params(C.Structure):
 class Bufs(C.Structure):
     _fields_ = [("near", _vp), ("far", _vp), ("coeffs", _vp), ("accum", _vp), ("weight", _vp),
                 ("refraction_offset", _vp), ("output", _vp), ("vhat", _vp),
-                ("full_opaque_image", _vp), ("diffusion", _vp), ("blurred_image", _vp)]
+                ("full_opaque_image", _vp), ("diffusion", _vp), ("blurred_image", _vp), ("coeff_words", _vp)]
 
 
 _d3 = C.c_double * 3

@@ -148,6 +148,7 @@ int woit_step2_build(const woit_frags_t* frags, const woit_params_t* params, woi
     b.near = bufs->near;
     b.far = bufs->far;
     b.coeffs = bufs->coeffs;
+    b.coeff_words = bufs->coeff_words;  // packed storage: the words of the accumulated coefficients
     return run_frame(frags, params, &b, PH_BUILD | PH_BUILD_ACC, ws, ws_bytes, stream);
 }
 

@@ -453,7 +453,7 @@ WOIT_D void empty_run(const KParams& kp, int flags, int64_t p0, int ne, int lane
     constexpr int V = 3 * (2 << R);
     if (kp.b.coeffs) {
         float* c = kp.b.coeffs + p0 * V;
-        const bool packed = GEN && (flags & WOIT_PACKED_STORAGE);
+        const bool packed = flags & WOIT_PACKED_STORAGE;
         if (V % 4 == 0 && (reinterpret_cast<uintptr_t>(c) & 15u) == 0) {
             constexpr int V4 = V / 4 > 0 ? V / 4 : 1;
             float4* c4 = reinterpret_cast<float4*>(c);
@@ -468,6 +468,10 @@ WOIT_D void empty_run(const KParams& kp, int flags, int64_t p0, int ne, int lane
         } else {
             for (int i = lane; i < ne * V; i += 32) c[i] = (packed && (i % V) >= 3) ? -0.0f : 0.0f;
         }
+    }
+    if ((flags & WOIT_PACKED_STORAGE) && kp.b.coeff_words) {
+        constexpr int S = 2 << R;  // E5B9G9R9 of zeros: word 0
+        for (int i = lane; i < ne * S; i += 32) kp.b.coeff_words[p0 * S + i] = 0u;
     }
     if (lane >= ne) return;
     const int64_t p = p0 + lane;
@@ -507,11 +511,11 @@ struct WSmem {
     float* normal;
     uint8_t* bf;
     zfix_t* zfix;      // [FBW] z in fixed point, by fragment
-    float* part;       // [V][32] chunk partials (f64 [WIN][V] scratch for packed storage)
+    float* part;       // [rows][3][32] chunk partials
     float2* cells;     // [SUBP][M][3] (v_c, v_{c+1} - v_c): staircase at cell centres
     float* coef32;     // [WIN][V] coefficients, bulk-stored to bufs->coeffs
     float* accp;       // [8][32] chunk accumulators
-    double* pk;        // [WIN][V] f64 coefficients for packed storage
+    uint32_t* words;   // [SUBP][S] E5B9G9R9 words of the sub-tile (packed storage)
     float* opq;        // [SUBP+4][3] staged opaque colours of the sub-tile (fast path)
     uint64_t* bar;
 };
@@ -537,7 +541,7 @@ WOIT_D WSmem<R, GEN> wcarve(unsigned char* base, const WLayout& L) {
     s.cells = reinterpret_cast<float2*>(base + L.cells);
     s.coef32 = reinterpret_cast<float*>(base + L.coef32);
     s.accp = reinterpret_cast<float*>(base + L.accp);
-    s.pk = reinterpret_cast<double*>(base + L.pk);
+    s.words = reinterpret_cast<uint32_t*>(base + L.words);
     s.opq = reinterpret_cast<float*>(base + L.opq);
     s.bar = reinterpret_cast<uint64_t*>(base + L.bar);
     return s;
@@ -546,8 +550,14 @@ WOIT_D WSmem<R, GEN> wcarve(unsigned char* base, const WLayout& L) {
 // FUS: the phases are the fused render's (compile-time constant), so the
 // step-wise accumulate / from-buffer branches compile out; GEN && !FUS serves the
 // step1..step4 entry points.
+// Minimum resident warps per SM the fast instances are compiled for (the register cap):
+// rank <= 3 hold 15 warps by shared memory; ranks 4-6 fewer (their partials and cell
+// tables are larger), so their register budget is looser and they do not spill.
+template <int R>
+constexpr int kMinWarps() { return R <= 3 ? WOIT_MINB : R == 4 ? 10 : R == 5 ? 6 : 4; }
+
 template <int R, bool GEN, bool FUS, int VAR, int FL>
-__global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R>::WPB) frame_kernel(const __grid_constant__ KParams kp) {
+__global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) / WT<R>::WPB) frame_kernel(const __grid_constant__ KParams kp) {
     using G = WT<R>;
     constexpr int S = G::S, V = G::V, CH = G::CH, WC = 32, FBW = G::FBW, WIN = G::WIN, SUBP = G::SUBP;
     constexpr int AR = WC + 1;  // chunk-accumulator row stride: the (pixel, channel) combine lanes hit distinct banks
@@ -559,7 +569,8 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const uint32_t ph = (GEN && !FUS) ? kp.phases : kFused;
     // FL != 0: an instance specialised for exactly these flags (all but NORMALIZE)
-    const int flags = GEN ? (FL ? (FL | (kp.p.flags & WOIT_NORMALIZE)) : kp.p.flags) : (kp.p.flags & WOIT_NORMALIZE);
+    // (the fast path's FL is WOIT_PACKED_STORAGE for its packed-storage instance, else 0)
+    const int flags = GEN ? (FL ? (FL | (kp.p.flags & WOIT_NORMALIZE)) : kp.p.flags) : ((kp.p.flags & WOIT_NORMALIZE) | FL);
     const WLayout L = make_wlayout<R>(ph, flags, !GEN && WOIT_ALIASZ);
     const int lane = threadIdx.x & 31;
     WSmem<R, GEN> sm = wcarve<R, GEN>(smem_raw + (threadIdx.x >> 5) * L.total, L);
@@ -606,7 +617,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
     const bool cube = GEN && (flags & WOIT_CUBE_TRANSMISSION);
     const bool bfonly = cube && (flags & WOIT_CUBE_BACKFACE_ONLY);
     const bool need_ior = do_at && (cube || refr);
-    const bool packed = GEN && (flags & WOIT_PACKED_STORAGE);
+    const bool packed = flags & WOIT_PACKED_STORAGE;
     const int64_t nalloc = kp.f.nfrag;
     // thin sub-tiles: the fused render without packed storage, when the coefficient
     // transpose ([V][33] floats) fits over the depth / alpha / T / L staging arrays
@@ -1370,8 +1381,8 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
             __syncwarp();
             if (task) {
                 const int q = q0 + kq;
-                if (do_eval) store_cells<M>(sm.cells, kq, kch, rc);
-                if (need_coef) sm.vtot[kq * 3 + kch] = expf(-rc[M - 1]);  // A(z -> 1) = v_{M-1}
+                if (do_eval && !packed) store_cells<M>(sm.cells, kq, kch, rc);
+                if (need_coef && !packed) sm.vtot[kq * 3 + kch] = expf(-rc[M - 1]);  // A(z -> 1) = v_{M-1}
                 // coefficients: Haar analysis of v in f64 (wavelet.py:3-9 layout):
                 // c[2^n + k] = 2^(n/2)/M (sum left half - sum right half), c[0] = mean
                 double T[M];
@@ -1383,44 +1394,44 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
                     for (int s = 0; s < S; ++s) c[s] = dadd(c[s], (double)kp.b.coeffs[(w0 + q) * V + 3 * s + kch]);
                 }
             }
-            if (!packed && task) {
+            if (task) {
 #pragma unroll
                 for (int s = 0; s < S; ++s) sm.coef32[kq * V + 3 * s + kch] = (float)c[s];
             }
-            if (GEN && packed && task) {
-                // the shared exponent couples the channels: stage the f64 coefficients
-#pragma unroll
-                for (int s = 0; s < S; ++s) sm.pk[kq * V + 3 * s + kch] = c[s];
-            }
-            if (GEN && packed) {
+            if (packed) {
+                // E5B9G9R9 storage (packing.py:46-111, pipeline.py:154-155): the shared
+                // exponent couples the channels, so each (pixel, slot) task packs the three
+                // fp32 coefficients just stored (fp32-valued inputs: every step of the
+                // reference's pack is exact), keeps the word and writes back the unpacked
+                // value m 2^(e-24) (exact in fp32) with the positional sign -- the values
+                // the evaluation, v_tot and the coefficient output then use
                 __syncwarp();
-                double* c64 = sm.pk;
                 for (int idx = lane; idx < nqs * S; idx += 32) {
-                    double* t3 = c64 + idx * 3;
-                    double mag[3] = {fabs(t3[0]), fabs(t3[1]), fabs(t3[2])}, rt[3];
-                    rgb9e5_unpack_impl(rgb9e5_pack_impl(mag), rt);
-                    const double sg = (idx % S) == 0 ? 1.0 : -1.0;
+                    const int pq = idx / S, sl = idx - pq * S;
+                    float* t3 = sm.coef32 + pq * V + 3 * sl;
+                    const uint32_t w = rgb9e5_pack_fp32(fabsf(t3[0]), fabsf(t3[1]), fabsf(t3[2]));
+                    float rt[3];
+                    rgb9e5_unpack_fp32(w, rt);
+                    sm.words[idx] = w;
+                    const float sg = sl == 0 ? 1.0f : -1.0f;
                     t3[0] = sg * rt[0];
                     t3[1] = sg * rt[1];
                     t3[2] = sg * rt[2];
                 }
                 __syncwarp();
-                for (int t = lane; t < nqs * 3; t += 32) {
-                    const int kch = t / nqs, kq = t - kch * nqs;
-                    double c[S];
+                if (task) {
+                    double cu[S];
 #pragma unroll
-                    for (int s = 0; s < S; ++s) c[s] = c64[kq * V + 3 * s + kch];
-#pragma unroll
-                    for (int s = 0; s < S; ++s) sm.coef32[kq * V + 3 * s + kch] = (float)c[s];
+                    for (int s = 0; s < S; ++s) cu[s] = (double)sm.coef32[kq * V + 3 * s + kch];
                     if (need_coef) {
-                        double at = c[0];
+                        double at = cu[0];
 #pragma unroll
-                        for (int n = 0; n <= R; ++n) at = dsub(at, dmul(kSqrt2Pow[n], c[(2 << n) - 1]));
+                        for (int n = 0; n <= R; ++n) at = dsub(at, dmul(kSqrt2Pow[n], cu[(2 << n) - 1]));
                         sm.vtot[kq * 3 + kch] = expf(-(float)fmax(at, 0.0));
                     }
                     if (do_eval) {
                         double cell[S];
-                        haar_cells<R>(c, cell);
+                        haar_cells<R>(cu, cell);
                         store_cells<M>(sm.cells, kq, kch, cell);
                     }
                 }
@@ -1441,8 +1452,20 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : WOIT_MINB) / WT<R
                 store_cells<M>(sm.cells, kq, kch, cell);
             }
         }
-        fence_proxy_async();  // coef32 becomes visible to the bulk store
+        fence_proxy_async();  // coef32 / words become visible to the bulk stores
         __syncwarp();
+        if (packed && (ph & PH_BUILD) && kp.b.coeff_words) {
+            uint32_t* g = kp.b.coeff_words + (w0 + q0) * S;
+            const uint32_t bytes = (uint32_t)(nqs * S * 4);
+            if (kp.use_tma && ((reinterpret_cast<uintptr_t>(g) & 15u) == 0) && (bytes & 15u) == 0) {
+                if (lane == 0) {
+                    bulk_s2g(g, sm.words, bytes);
+                    bulk_commit();
+                }
+            } else {
+                for (int i = lane; i < nqs * S; i += 32) g[i] = sm.words[i];
+            }
+        }
         if ((ph & PH_BUILD) && kp.b.coeffs) {
             float* g = kp.b.coeffs + (w0 + q0) * V;
             const uint32_t bytes = (uint32_t)(nqs * V * 4);
@@ -1670,11 +1693,15 @@ __global__ void __launch_bounds__(kLongT) long_pixel_kernel(const __grid_constan
             }
             __syncthreads();
             if (flags & WOIT_PACKED_STORAGE) {
+                // the frame kernel's packing: the fp32 coefficients, packed and unpacked
                 for (int sl = tid; sl < S; sl += kLongT) {
-                    double mag[3] = {fabs(coef[3 * sl]), fabs(coef[3 * sl + 1]), fabs(coef[3 * sl + 2])}, rt[3];
-                    rgb9e5_unpack_impl(rgb9e5_pack_impl(mag), rt);
+                    const uint32_t w = rgb9e5_pack_fp32(fabsf((float)coef[3 * sl]), fabsf((float)coef[3 * sl + 1]),
+                                                        fabsf((float)coef[3 * sl + 2]));
+                    float rt[3];
+                    rgb9e5_unpack_fp32(w, rt);
+                    if (kp.b.coeff_words) kp.b.coeff_words[p * S + sl] = w;
                     const double sg = sl == 0 ? 1.0 : -1.0;
-                    for (int ch = 0; ch < 3; ++ch) coef[3 * sl + ch] = sg * rt[ch];
+                    for (int ch = 0; ch < 3; ++ch) coef[3 * sl + ch] = sg * (double)rt[ch];
                 }
                 __syncthreads();
             }
@@ -1838,7 +1865,7 @@ template <int R, bool GEN, bool FUS, int VAR, int FL = 0>
 cudaError_t launch_tiles(const KParams& kp, cudaStream_t st) {
     using G = WT<R>;
     const uint32_t ph = (GEN && !FUS) ? kp.phases : (PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE);
-    const WLayout L = make_wlayout<R>(ph, GEN ? kp.p.flags : (kp.p.flags & WOIT_NORMALIZE), !GEN && WOIT_ALIASZ);
+    const WLayout L = make_wlayout<R>(ph, GEN ? kp.p.flags : ((kp.p.flags & WOIT_NORMALIZE) | FL), !GEN && WOIT_ALIASZ);
     const int bytes = (int)(L.total * G::WPB);
     // persistent grid: as many CTAs as can be resident, each warp loops over windows
     const int64_t warps = (kp.f.npix + G::WIN - 1) / G::WIN;
@@ -1881,6 +1908,9 @@ cudaError_t launch_rank(const KParams& kp, cudaStream_t st) {
     constexpr uint32_t kFused = PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE;
     const bool fused = kp.phases == kFused;
     const bool fast = fused && (kp.p.flags & ~WOIT_NORMALIZE) == 0;
+    // packed storage alone: the fast kernel with the E5B9G9R9 epilogue (plain sub-tiles
+    // at every depth); rank 0 (8-byte words per pixel pair) takes the general kernel
+    const bool fast_packed = R >= 1 && fused && (kp.p.flags & ~WOIT_NORMALIZE) == WOIT_PACKED_STORAGE;
     // thin sub-tiles are compiled into a separate instance of the fast kernel: their
     // code measurably slows the deep-pixel instance even when no thin sub-tile forms
     // (the two give identical bits, so the choice is only a matter of speed)
@@ -1889,7 +1919,8 @@ cudaError_t launch_rank(const KParams& kp, cudaStream_t st) {
     // average): it pays at 256 fragments per pixel and costs the others codegen.
     const bool shallow = WOIT_THIN && kp.f.nfrag <= 16 * kp.f.npix;
     const bool deep = kp.f.nfrag > 160 * kp.f.npix;
-    cudaError_t err = fast ? (shallow ? launch_tiles<R, false, true, kVarThin>(kp, st)
+    cudaError_t err = fast_packed ? launch_tiles<R, false, true, kVarPlain, WOIT_PACKED_STORAGE>(kp, st)
+                      : fast ? (shallow ? launch_tiles<R, false, true, kVarThin>(kp, st)
                               : deep  ? launch_tiles<R, false, true, kVarDeep>(kp, st)
                                       : launch_tiles<R, false, true, kVarPlain>(kp, st))
                            : fused ? launch_general<R>(kp, st)

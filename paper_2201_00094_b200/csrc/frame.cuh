@@ -68,7 +68,7 @@ struct WT {
 
 struct WLayout {
     uint32_t offs, cb, lo, den, rcp, vtot;
-    uint32_t depth, alpha, trans, rad, ior, normal, bf, zfix, part, cells, coef32, accp, pk, opq, bar, total;
+    uint32_t depth, alpha, trans, rad, ior, normal, bf, zfix, part, cells, coef32, accp, words, opq, bar, total;
 };
 
 WOIT_HD uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
@@ -126,13 +126,15 @@ WOIT_HD WLayout make_wlayout(uint32_t phases, int flags, bool alias_z) {
     const uint32_t part_b = (phases & PH_BUILD) ? 4u * 3 * 32 * PartRows<R>::n(tight) : 0u;
     const uint32_t cells_b = (uint32_t)G::SUBP * (G::S + 1) * 24u;  // frame.cu CellTab
     const uint32_t acc_b = ev ? align16(4u * (alias_z ? 6 : 9) * 33) : 0u;  // rows of 33 (frame.cu AR)
-    const uint32_t after_b = align16(4u * G::SUBP * G::V) + align16(cells_b) + acc_b + (alias_z ? 4u * 3 * G::SUBP : 0u);
+    const uint32_t vtot_b = alias_z ? align16(4u * 3 * G::SUBP) : 0u;
+    const uint32_t words_b = packed ? align16(4u * G::SUBP * G::S) : 0u;  // E5B9G9R9 words of the sub-tile
+    const uint32_t after_b = align16(4u * G::SUBP * G::V) + align16(cells_b) + acc_b + vtot_b + words_b;
     L.part = o;  o = align16(o + (part_b > after_b ? part_b : after_b));
     L.coef32 = L.part;
     L.cells = L.part + align16(4u * G::SUBP * G::V);
     L.accp = L.cells + align16(cells_b);
     if (alias_z) L.vtot = L.accp + acc_b;
-    L.pk = o;    o = align16(o + (packed ? 8u * G::WIN * G::V : 0u));
+    L.words = L.accp + acc_b + vtot_b;
     L.opq = o;   o = align16(o + 12u * (G::SUBP + 4));  // [pa & ~3, pb rounded up to 4)
     L.bar = o;   o = align16(o + 16u);
 #ifdef WOIT_SMEM_PAD

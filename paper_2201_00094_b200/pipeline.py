@@ -160,9 +160,13 @@ class FrameBuffers:
     output: torch.Tensor
     vhat: Optional[torch.Tensor] = None  # per-fragment transmittance (filled by step3 / render)
     diffusion: Optional[torch.Tensor] = None  # per-pixel coverage D_p (WOIT_DIFFUSION)
+    # packed storage (cfg.packed_storage): [P][S] E5B9G9R9 words (packing.py:46-77), int32
+    # tensor holding the uint32 bit patterns -- the paper's 4 S bytes per pixel
+    coeff_words: Optional[torch.Tensor] = None
 
     @classmethod
-    def allocate(cls, frame: FrameFragments, rank: int, vhat: bool = False) -> "FrameBuffers":
+    def allocate(cls, frame: FrameFragments, rank: int, vhat: bool = False,
+                 packed: bool = False) -> "FrameBuffers":
         P, dev = frame.npix, frame.device
         z = lambda *s: torch.zeros(*s, dtype=torch.float32, device=dev)
         return cls(frame.width, frame.height, rank,
@@ -170,7 +174,8 @@ class FrameBuffers:
                    torch.full((P,), -math.inf, dtype=torch.float32, device=dev),
                    z(P, 1 << (rank + 1), 3), z(P, 3), z(P, 3), z(P, 2),
                    frame.opaque_depth.clone(), frame.opaque_color.clone(), z(P, 3),
-                   z(frame.nfrag, 3) if vhat else None, z(P))
+                   z(frame.nfrag, 3) if vhat else None, z(P),
+                   torch.zeros(P, 1 << (rank + 1), dtype=torch.int32, device=dev) if packed else None)
 
     def image(self) -> torch.Tensor:
         return self.output.reshape(-1, self.width, 3)
@@ -191,6 +196,7 @@ class FrameBuffers:
             blurred_image = blurred_image.to(torch.float32).contiguous()
             self._blur_keepalive = blurred_image
         b.blurred_image = ptr(blurred_image)
+        b.coeff_words = ptr(self.coeff_words)
         return b
 
 
@@ -394,7 +400,7 @@ def render_band(frame: FrameFragments, cfg: RenderConfig, rays: Optional[RayGrid
     """
     lib = _lib.load()
     if bufs is None:
-        bufs = FrameBuffers.allocate(frame, cfg.rank, vhat=vhat)
+        bufs = FrameBuffers.allocate(frame, cfg.rank, vhat=vhat, packed=cfg.packed_storage)
     _check_frame(frame, bufs)
     if cfg.diffusion > 0.0 and blurred_image is None:
         blurred_image = resolve_blur(_background_image(frame, full_opaque_image), cfg.diffusion_radius)

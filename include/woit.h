@@ -294,11 +294,23 @@ int woit_total_absorbance(const double* coeffs, int64_t npix, int rank, double* 
 
 size_t woit_bin_workspace_bytes(int64_t n, int64_t npix);
 
-/* Stable counting sort of fragment ids by pixel: offsets[npix+1] equals
- * concatenate([0], cumsum(bincount(pix, minlength=npix))) and perm lists the
- * fragment ids of each pixel in their original order (np.argsort(pix, kind="stable")). */
+/* Stable sort of fragment ids by pixel (an LSD radix sort: one stable counting sort --
+ * digit histogram per tile, scan, stable scatter -- per 8 bits of the pixel id, over
+ * ceil(log2 npix) bits): offsets[npix+1] equals concatenate([0], cumsum(bincount(pix,
+ * minlength=npix))) and perm lists the fragment ids of each pixel in their original
+ * order (np.argsort(pix, kind="stable")). pix in [0, npix); n, npix < 2^31. */
 int woit_bin_by_pixel(const int64_t* pix, int64_t n, int64_t npix, int64_t* offsets,
                       int64_t* perm, void* ws, size_t ws_bytes, void* stream);
+
+/* An unbinned stream -> the CSR stream the frame kernels take (scene.py:559-566): the
+ * same stable sort, with the last pass scattering every fragment's fields (depth,
+ * alpha, trans, radiance, normal, ior, backface -- each present on both sides or
+ * neither) straight from its arrival slot into its CSR slot. unbinned->nfrag / npix
+ * give the sizes (unbinned->offsets unused); binned's field pointers are the outputs
+ * (its const qualifiers notwithstanding); offsets int64[npix+1]; perm int64[n] or NULL. */
+size_t woit_bin_frame_workspace_bytes(int64_t n, int64_t npix);
+int woit_bin_frame(const int32_t* pix, const woit_frags_t* unbinned, woit_frags_t* binned, int64_t* offsets,
+                   int64_t* perm, void* ws, size_t ws_bytes, void* stream);
 
 /* ---- E5B9G9R9 packing (packing.py:46-111) --------------------------------- */
 

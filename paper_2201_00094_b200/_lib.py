@@ -114,6 +114,8 @@ _SIGS = {
     "woit_total_absorbance": (C.c_int, [_vp, _i64, C.c_int, _vp, _vp]),
     "woit_bin_workspace_bytes": (_sz, [_i64, _i64]),
     "woit_bin_by_pixel": (C.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "woit_bin_frame_workspace_bytes": (_sz, [_i64, _i64]),
+    "woit_bin_frame": (C.c_int, [_vp, C.POINTER(Frags), C.POINTER(Frags), _vp, _vp, _vp, _sz, _vp]),
     "woit_pack_rgb9e5": (C.c_int, [_vp, _i64, _vp, _vp]),
     "woit_unpack_rgb9e5": (C.c_int, [_vp, _i64, _vp, _vp]),
     "woit_synth_workspace_bytes": (_sz, [_i64]),

@@ -20,7 +20,7 @@ REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(REPO, "build")
 LIB = os.path.join(PKG, "libwoit.so")
-SOURCES = ("frame.cu", "batch.cu", "synth.cu", "resolve.cu", "build_atomic.cu", "baselines.cu", "cast.cu", "abi.cu")
+SOURCES = ("frame.cu", "batch.cu", "binning.cu", "synth.cu", "resolve.cu", "build_atomic.cu", "baselines.cu", "cast.cu", "abi.cu")
 HEADERS = ("common.cuh", "frame.cuh", "packing.cuh", "internal.cuh")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -312,8 +312,27 @@ size_t woit_bin_workspace_bytes(int64_t n, int64_t npix) { return bin_workspace(
 int woit_bin_by_pixel(const int64_t* pix, int64_t n, int64_t npix, int64_t* offsets, int64_t* perm, void* ws,
                       size_t ws_bytes, void* stream) {
     if (n < 0 || npix < 0 || !offsets || (n > 0 && (!pix || !perm))) return WOIT_EINVAL;
+    if (n >= ((int64_t)1 << 31) || npix >= ((int64_t)1 << 31)) return WOIT_EINVAL;
     if (n > 0 && (!ws || ws_bytes < bin_workspace(n, npix))) return WOIT_EWORKSPACE;
     return cuda_status(bin_by_pixel(pix, n, npix, offsets, perm, ws, ws_bytes, static_cast<cudaStream_t>(stream)));
+}
+
+size_t woit_bin_frame_workspace_bytes(int64_t n, int64_t npix) { return n < 0 || npix < 0 ? 0 : bin_workspace(n, npix); }
+
+int woit_bin_frame(const int32_t* pix, const woit_frags_t* unbinned, woit_frags_t* binned, int64_t* offsets,
+                   int64_t* perm, void* ws, size_t ws_bytes, void* stream) {
+    if (!unbinned || !binned || !offsets) return WOIT_EINVAL;
+    const int64_t n = unbinned->nfrag, npix = unbinned->npix;
+    if (n < 0 || npix < 1 || n >= ((int64_t)1 << 31) || npix >= ((int64_t)1 << 31)) return WOIT_EINVAL;
+    if (n > 0 && (!pix || !unbinned->depth || !binned->depth)) return WOIT_EINVAL;
+    // every optional field travels iff both sides have it
+    const void* pairs[][2] = {{unbinned->alpha, binned->alpha}, {unbinned->trans, binned->trans},
+                              {unbinned->radiance, binned->radiance}, {unbinned->normal, binned->normal},
+                              {unbinned->ior, binned->ior}, {unbinned->backface, binned->backface}};
+    for (auto& pr : pairs)
+        if ((pr[0] == nullptr) != (pr[1] == nullptr)) return WOIT_EINVAL;
+    if (n > 0 && (!ws || ws_bytes < bin_workspace(n, npix))) return WOIT_EWORKSPACE;
+    return cuda_status(bin_frame(pix, n, npix, *unbinned, *binned, offsets, perm, ws, static_cast<cudaStream_t>(stream)));
 }
 
 int woit_pack_rgb9e5(const double* v, int64_t n, uint32_t* words, void* stream) {

@@ -1,72 +1,13 @@
 // Kernel-level batch entry points (wavelet.py:272-337), fragment binning, and
 // E5B9G9R9 packing (packing.py:46-111). float64 like the reference; the binned
 // build reproduces np.add.at's per-slot addition order exactly.
-#include <cub/device/device_radix_sort.cuh>
-
 #include "common.cuh"
 #include "internal.cuh"
 #include "packing.cuh"
 
 namespace woit {
 
-// --- binning ---------------------------------------------------------------
-
-__global__ void iota_kernel(int64_t* v, int64_t n) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        v[i] = i;
-}
-
-// offsets[p] = lower_bound(sorted_keys, p) for p in [0, npix]
-__global__ void offsets_from_sorted(const int64_t* keys, int64_t n, int64_t npix, int64_t* offsets) {
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p <= npix;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        int64_t lo = 0, hi = n;
-        while (lo < hi) {
-            const int64_t mid = (lo + hi) >> 1;
-            if (keys[mid] < p) lo = mid + 1; else hi = mid;
-        }
-        offsets[p] = lo;
-    }
-}
-
-static int key_bits(int64_t npix) {
-    int b = 1;
-    while (b < 63 && (int64_t(1) << b) < npix) ++b;
-    return b;
-}
-
-size_t bin_workspace(int64_t n, int64_t npix) {
-    size_t temp = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, temp, (const int64_t*)nullptr, (int64_t*)nullptr,
-                                    (const int64_t*)nullptr, (int64_t*)nullptr, (int)(n > 0 ? n : 1),
-                                    0, key_bits(npix));
-    return ((temp + 255) & ~(size_t)255) + 2 * (size_t)(n > 0 ? n : 1) * 8 + 256;
-}
-
-cudaError_t bin_by_pixel(const int64_t* pix, int64_t n, int64_t npix, int64_t* offsets, int64_t* perm,
-                         void* ws, size_t ws_bytes, cudaStream_t st) {
-    if (n == 0) {
-        return cudaMemsetAsync(offsets, 0, (size_t)(npix + 1) * 8, st);
-    }
-    size_t temp = 0;
-    const int bits = key_bits(npix);
-    cub::DeviceRadixSort::SortPairs(nullptr, temp, pix, (int64_t*)nullptr, (const int64_t*)nullptr,
-                                    perm, (int)n, 0, bits, st);
-    unsigned char* w = static_cast<unsigned char*>(ws);
-    const size_t temp_al = (temp + 255) & ~(size_t)255;
-    int64_t* keys_out = reinterpret_cast<int64_t*>(w + temp_al);
-    int64_t* ids = keys_out + n;
-    const int grid = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
-    iota_kernel<<<grid, 256, 0, st>>>(ids, n);
-    cudaError_t err = cub::DeviceRadixSort::SortPairs(w, temp, pix, keys_out, ids, perm, (int)n, 0,
-                                                      bits, st);
-    if (err != cudaSuccess) return err;
-    const int g2 = (int)((npix + 256) / 256 < 4096 ? (npix + 256) / 256 : 4096);
-    offsets_from_sorted<<<g2, 256, 0, st>>>(keys_out, n, npix, offsets);
-    (void)ws_bytes;
-    return cudaGetLastError();
-}
+// --- binning: csrc/binning.cu (bin_by_pixel, bin_workspace) ---
 
 // --- build_into ----------------------------------------------------------------
 

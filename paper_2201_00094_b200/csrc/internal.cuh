@@ -11,6 +11,8 @@ cudaError_t launch_indices(const KParams& kp, double* z, int32_t* k, int32_t* ce
 size_t bin_workspace(int64_t n, int64_t npix);
 cudaError_t bin_by_pixel(const int64_t* pix, int64_t n, int64_t npix, int64_t* offsets, int64_t* perm,
                          void* ws, size_t ws_bytes, cudaStream_t st);
+cudaError_t bin_frame(const int32_t* pix, int64_t n, int64_t npix, const woit_frags_t& in, const woit_frags_t& out,
+                      int64_t* offsets, int64_t* perm, void* ws, cudaStream_t st);
 size_t build_into_workspace(int64_t n, int64_t npix);
 cudaError_t build_into(double* coeffs, int64_t npix, const int64_t* pix, const double* z, const double* a,
                        int64_t n, int rank, int mode, void* ws, size_t ws_bytes, cudaStream_t st);

@@ -147,6 +147,51 @@ class FrameFragments:
         return cls(width, height, offsets, depth, alpha, trans, rad, normal, ior, bf, od, oc,
                    row0 * width, frag_base)
 
+    @classmethod
+    def from_unbinned(cls, width: int, height: int, pix: torch.Tensor, depth: torch.Tensor, alpha: torch.Tensor,
+                      trans: torch.Tensor, radiance: torch.Tensor, normal: Optional[torch.Tensor] = None,
+                      ior: Optional[torch.Tensor] = None, backface: Optional[torch.Tensor] = None,
+                      opaque_depth: Optional[torch.Tensor] = None, opaque_color: Optional[torch.Tensor] = None,
+                      npix: Optional[int] = None, pixel_base: int = 0, return_perm: bool = False):
+        """CSR stream from an unbinned one (the producer's arrival order, a pixel id per
+        fragment): ``woit_bin_frame`` -- a stable sort by pixel whose last pass scatters
+        every fragment's fields into its CSR slot (scene.py:559-566: offsets =
+        cumsum(bincount), each pixel's fragments in arrival order). Device tensors in,
+        device tensors out; with ``return_perm`` also argsort(pix, kind="stable")."""
+        dev = depth.device
+        lib = _lib.load()
+        n = depth.numel()
+        P = width * height if npix is None else npix
+        if pix.dtype != torch.int32 or pix.numel() != n or pix.device != dev:
+            raise ValueError("pix must be an int32 device tensor with one pixel id per fragment")
+        f32 = lambda t, *shape: t.to(dev, torch.float32).contiguous().reshape(*shape)
+        if normal is None:
+            normal = torch.tensor([0.0, 0.0, -1.0], device=dev).repeat(n, 1)
+        if ior is None:
+            ior = torch.ones(n, device=dev)
+        if backface is None:
+            backface = torch.zeros(n, dtype=torch.uint8, device=dev)
+        ins = dict(depth=f32(depth, n), alpha=f32(alpha, n), trans=f32(trans, n, 3), radiance=f32(radiance, n, 3),
+                   normal=f32(normal, n, 3), ior=f32(ior, n), backface=backface.to(dev, torch.uint8).contiguous())
+        outs = {k: torch.empty_like(v) for k, v in ins.items()}
+        offsets = torch.empty(P + 1, dtype=torch.int64, device=dev)
+        perm = torch.empty(max(n, 1), dtype=torch.int64, device=dev) if return_perm else None
+        fi, fo = _lib.Frags(), _lib.Frags()
+        for f, d in ((fi, ins), (fo, outs)):
+            f.width, f.height, f.npix, f.nfrag = width, height, P, n
+            for k, v in d.items():
+                setattr(f, k, ptr(v))
+        wsn = lib.woit_bin_frame_workspace_bytes(n, P)
+        ws = torch.empty(max(wsn, 1), dtype=torch.uint8, device=dev)
+        with torch.cuda.device(dev):
+            _lib.check(lib.woit_bin_frame(ptr(pix), fi, fo, ptr(offsets), ptr(perm), ptr(ws), wsn, _stream()),
+                       "woit_bin_frame")
+        od = opaque_depth if opaque_depth is not None else torch.full((P,), float("inf"), device=dev)
+        oc = opaque_color if opaque_color is not None else torch.zeros(P, 3, device=dev)
+        frame = cls(width, height, offsets, outs["depth"], outs["alpha"], outs["trans"], outs["radiance"],
+                    outs["normal"], outs["ior"], outs["backface"], f32(od, P), f32(oc, P, 3), pixel_base, 0)
+        return (frame, perm[:n]) if return_perm else frame
+
     # -- views --------------------------------------------------------------------
 
     def band(self, p0: int, p1: int) -> "FrameFragments":

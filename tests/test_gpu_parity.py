@@ -462,3 +462,44 @@ def test_config2_full_size_properties(W):
         assert np.abs(h(bufs.vhat[f0:f1]) - ref.vhat).max() <= VHAT_TOL
         assert np.abs(h(bufs.accum[p0:p1]) - ref.accum).max() <= IMG_TOL
         assert np.abs(h(bufs.output[p0:p1]) - ref.output).max() <= IMG_TOL
+
+
+@pytest.mark.parametrize("workload,w,hgt,layers", [("ragged", 61, 37, 40), ("smoke", 96, 64, 32), ("plane4", 300, 1, 5)])
+def test_bin_frame_is_the_reference_csr(W, workload, w, hgt, layers):
+    """woit_bin_frame on a shuffled (unbinned) stream: offsets = cumsum(bincount), the
+    fields of each pixel in arrival order (np.argsort(kind="stable"), scene.py:559-566),
+    and the render of the binned stream equals the render of the original CSR stream."""
+    sf = W.synth.generate(workload, w, hgt, seed=9, layers=layers)
+    frame = W.FrameFragments.from_synth(sf)
+    n, P = frame.nfrag, frame.npix
+    order = torch.randperm(n, device="cuda", generator=torch.Generator(device="cuda").manual_seed(3))
+    pix = W.pixel_ids(frame)[order].contiguous()
+    fb, perm = W.FrameFragments.from_unbinned(w, hgt, pix, frame.depth[order], frame.alpha[order],
+                                              frame.trans[order], frame.radiance[order], frame.normal[order],
+                                              frame.ior[order], frame.backface[order], frame.opaque_depth,
+                                              frame.opaque_color, return_perm=True)
+    torch.cuda.synchronize()
+    p_np = pix.cpu().numpy()
+    want_perm = np.argsort(p_np, kind="stable")
+    np.testing.assert_array_equal(perm.cpu().numpy(), want_perm)
+    np.testing.assert_array_equal(fb.offsets.cpu().numpy(),
+                                  np.concatenate([[0], np.cumsum(np.bincount(p_np, minlength=P))]))
+    for name in ("depth", "alpha", "trans", "radiance", "normal", "ior", "backface"):
+        np.testing.assert_array_equal(getattr(fb, name).cpu().numpy(),
+                                      getattr(frame, name)[order].cpu().numpy()[want_perm], name)
+    cfg = W.RenderConfig(rank=3, width=w, height=hgt)
+    a = W.render_band(frame, cfg)
+    b = W.render_band(fb, cfg)
+    torch.cuda.synchronize()
+    # same fragments per pixel, a different within-pixel order: order independence
+    assert float((a.output - b.output).abs().max()) < 1e-5
+
+
+@pytest.mark.parametrize("P,n", [(1, 1000), (256, 3), (257, 100000), (70000, 1 << 20), (2_073_600, 3_000_000)])
+def test_binning_sizes(W, P, n):
+    """Key widths of 0-21 bits (1-3 radix passes), tiny and ragged tiles, empty pixels."""
+    rng = np.random.default_rng(P + n)
+    pix = rng.integers(0, P, n)
+    offsets, perm = W.bin_by_pixel(pix, P)
+    np.testing.assert_array_equal(offsets.cpu().numpy(), np.concatenate([[0], np.cumsum(np.bincount(pix, minlength=P))]))
+    np.testing.assert_array_equal(perm.cpu().numpy(), np.argsort(pix, kind="stable"))

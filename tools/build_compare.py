@@ -12,6 +12,10 @@ stream after warm-up (median of --iters):
   bin_gather     permuting depth/alpha/T into CSR order (what binning an unbinned
                  stream costs before the tile build)
   fused_frame    woit_render_band: bounds+build+eval+composite in one launch
+  bin_frame_{layer_major,random}  woit_bin_frame on an unbinned stream (layer-major
+                 arrival, or a random permutation): the hand-written stable sort whose
+                 last pass scatters depth/alpha/T/L into CSR order
+  unbinned_*_to_rendered  woit_bin_frame + woit_render_band (unbinned stream -> image)
 and prints one JSON object. Coefficient agreement between the two builds is
 reported as max |diff|.
 """
@@ -105,4 +109,39 @@ res["atomic_unbinned_vs_tile_max_abs"] = float((bufs.coeffs - tile).abs().max())
 out = W.FrameBuffers.allocate(frame, args.rank)
 full = frame.opaque_color.reshape(args.height, args.width, 3)
 res["fused_frame_ms"] = timed(lambda: W.render_band(frame, cfg, bufs=out, full_opaque_image=full))
+
+# the hand-written binning (woit_bin_frame): stable radix sort by pixel whose last pass
+# scatters the fields into CSR order, then the fused frame on the binned stream. Two
+# arrival orders: layer-major (a producer emitting one layer of the whole frame after
+# another -- SURVEY.md §8(d)'s unbinned order) and a uniformly random permutation.
+run = frame.offsets[1:] - frame.offsets[:-1]
+L = int(run.max())
+lm = (frame.offsets[:-1][None, :] + torch.arange(L, device="cuda")[:, None])  # [layer][pixel] CSR index
+lm = lm[torch.arange(L, device="cuda")[:, None] < run[None, :]].contiguous()  # layer-major arrival order
+for tag, od in (("layer_major", lm), ("random", order)):
+    pix32 = pix[od].contiguous()
+    ins = dict(depth=frame.depth[od], alpha=frame.alpha[od], trans=frame.trans[od], radiance=frame.radiance[od])
+    outs = {k: torch.empty_like(v) for k, v in ins.items()}
+    fi, fo = _lib.Frags(), _lib.Frags()
+    for f, dd in ((fi, ins), (fo, outs)):
+        f.width, f.height, f.npix, f.nfrag = args.width, args.height, P, n
+        for k, v in dd.items():
+            setattr(f, k, ptr(v))
+    offs2 = torch.empty(P + 1, dtype=torch.int64, device="cuda")
+    wsn2 = lib.woit_bin_frame_workspace_bytes(n, P)
+    ws2 = torch.empty(wsn2, dtype=torch.uint8, device="cuda")
+    bin_frame = lambda: _lib.check(lib.woit_bin_frame(ptr(pix32), fi, fo, ptr(offs2), None, ptr(ws2), wsn2,
+                                                      st.cuda_stream), "bin_frame")
+    res[f"bin_frame_{tag}_ms"] = timed(bin_frame)
+    res[f"bin_frame_{tag}_offsets_equal"] = bool(torch.equal(offs2, frame.offsets))
+    fb = W.FrameFragments(width=args.width, height=args.height, offsets=offs2, depth=outs["depth"],
+                          alpha=outs["alpha"], trans=outs["trans"], radiance=outs["radiance"], normal=frame.normal,
+                          ior=frame.ior, backface=frame.backface, opaque_depth=frame.opaque_depth,
+                          opaque_color=frame.opaque_color)
+    out2 = W.FrameBuffers.allocate(frame, args.rank)
+    res[f"unbinned_{tag}_to_rendered_ms"] = timed(lambda: (bin_frame(), W.render_band(fb, cfg, bufs=out2,
+                                                                                      full_opaque_image=full)))
+    res[f"unbinned_{tag}_render_vs_csr_max_abs"] = float((out2.output - out.output).abs().max())
+    del ins, outs, ws2
+    torch.cuda.empty_cache()
 print(json.dumps(res))

@@ -50,6 +50,12 @@
 #ifndef WOIT_GEN_DYN  // dynamic window claims in the general kernel
 #define WOIT_GEN_DYN 1
 #endif
+#ifndef WOIT_GEN_PIPE  // pipelined window claims in the flag-specialised general instances
+#define WOIT_GEN_PIPE 1
+#endif
+#ifndef WOIT_EMPTY_DIRECT  // empty pixels of the general kernel take the background directly
+#define WOIT_EMPTY_DIRECT 1
+#endif
 #ifndef WOIT_PERSIST  // resident CTAs per SM slot multiplier for the persistent grid (0: one CTA per 2 windows)
 #define WOIT_PERSIST 1
 #endif
@@ -488,10 +494,26 @@ WOIT_D void empty_run(const KParams& kp, int flags, int64_t p0, int ne, int lane
     }
     if (GEN && (flags & WOIT_DIFFUSION) && kp.b.diffusion) kp.b.diffusion[p] = 0.0f;
     if (kp.b.output) {
+        // no fragments: v_tot = 1, acc = wgt = 0 and a zero refraction offset, so the
+        // composite returns the background sample exactly -- the pixel's own colour
+        // (the full image's at its global id when refraction / aberration gather from
+        // it, whose zero-offset sample is the pixel itself for 0/1 tap weights)
+        const bool gather = flags & (WOIT_CHROMATIC_ABERRATION | WOIT_REFRACTION);
+        const bool direct = !GEN || (WOIT_EMPTY_DIRECT && !(flags & WOIT_DIFFUSION) &&
+                                     (!(flags & WOIT_CHROMATIC_ABERRATION) ||
+                                      (kp.taps.n == kp.p.aberration_taps && kp.taps.unit)));
+        if (direct) {
+            const bool full = GEN && gather && kp.b.full_opaque_image;
+            const float* img = full ? kp.b.full_opaque_image + (kp.f.pixel_base + p) * 3 : kp.f.opaque_color + p * 3;
+            const float r = img[0], g = img[1], b = img[2];
+            kp.b.output[p * 3] = r;
+            kp.b.output[p * 3 + 1] = g;
+            kp.b.output[p * 3 + 2] = b;
+        } else {
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch)
-            kp.b.output[p * 3 + ch] = GEN ? composite_channel(kp, flags, p, ch, 0.0, 0.0, 0.0, 0.0, 1.0, 0.0)
-                                          : kp.f.opaque_color[p * 3 + ch];
+            for (int ch = 0; ch < 3; ++ch)
+                kp.b.output[p * 3 + ch] = composite_channel(kp, flags, p, ch, 0.0, 0.0, 0.0, 0.0, 1.0, 0.0);
+        }
     }
 }
 
@@ -590,7 +612,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
     // register spills in the generic instance, costs occupancy in the specialised ones.)
 #if WOIT_DYN
     unsigned long long claim_raw = 0;
-    constexpr bool kPipeClaims = !GEN;
+    constexpr bool kPipeClaims = !GEN || (WOIT_GEN_PIPE && FL != 0);
     if (kPipeClaims && lane == 0) claim_raw = atomicAdd(kp.win_counter, 1ull);
 #endif
     auto claim = [&]() -> int64_t {

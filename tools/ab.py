@@ -37,6 +37,29 @@ def child(cfg, iters):
     import torch
     import paper_2201_00094_b200 as W
     from paper_2201_00094_b200 import _lib
+    if cfg == "3":  # config 3: the wine-bottle preset cast on the device, refraction + CA + cube
+        from paper_2201_00094_b200.scene import cast_frame, preset
+        sc = preset("wine-bottle")
+        w, h, rank = 1920, 1080, 3
+        frame = cast_frame(sc, w, h)
+        cfgo = W.RenderConfig(rank=3, width=w, height=h, refraction=True, chromatic_aberration=True,
+                              cube_transmission=True)
+        rays = W.camera_rays(sc.camera, w, h)
+        full = frame.opaque_color.reshape(h, w, 3)
+        bufs = W.FrameBuffers.allocate(frame, 3)
+        ws = W.Workspace()
+        run = lambda: W.render_band(frame, cfgo, rays, bufs=bufs, full_opaque_image=full, ws=ws)
+        for _ in range(5):
+            run()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(iters):
+            run()
+        b.record()
+        torch.cuda.synchronize()
+        print(json.dumps({"ms": a.elapsed_time(b) / iters, "checksum": float(bufs.output.double().sum())}))
+        return
     wl, w, h, layers, rank = CFG[cfg]
     frame = W.FrameFragments.synthetic(wl, w, h, seed=1, layers=layers)
     cfgo = W.RenderConfig(rank=rank, width=w, height=h)

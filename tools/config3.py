@@ -5,7 +5,7 @@ refraction + chromatic aberration (k = 5) + cubed transmission, on one B200.
 
 Input: data/config3_wine_1080p.npz from tools/make_config3.py (the reference's
 own cast_frame output, fp32). Prints one JSON object: the GPU frame time (CUDA
-events, inputs resident, median of --iters after 3 warm-ups) of the general
+events, inputs resident, median over 3 batches of --iters back-to-back launches, as bench.py times steps) of the general
 (GEN) fused kernel, the same with the in-repo diffusion on (K_resolve blur +
 frame), roofline numbers with SURVEY.md §8(d)'s config-3 byte count, and the
 max |error| of coefficients / v̂ / image against the float64 oracle run on the
@@ -65,22 +65,28 @@ def main():
     bufs = W.FrameBuffers.allocate(frame, cfg.rank, vhat=True)
     st = torch.cuda.current_stream()
 
-    def timed(fn):
+    def timed(fn, batches=3):
+        """Median over batches of back-to-back launches (CUDA events around each batch
+        on the launching stream), as bench.py times its steps."""
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
         ts = []
-        for i in range(args.iters + 3):
+        for _ in range(batches):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(st)
-            fn()
+            for _ in range(args.iters):
+                fn()
             b.record(st)
             torch.cuda.synchronize()
-            if i >= 3:
-                ts.append(a.elapsed_time(b))
+            ts.append(a.elapsed_time(b) / args.iters)
         return float(np.median(ts))
 
-    ms = timed(lambda: W.render_band(frame, cfg, rays, bufs=bufs, full_opaque_image=full))
+    ws = W.Workspace()
+    ms = timed(lambda: W.render_band(frame, cfg, rays, bufs=bufs, full_opaque_image=full, ws=ws))
     dcfg = W.RenderConfig(width=Wd, height=H, diffusion=0.5, diffusion_radius=4, **CFG)
     dbufs = W.FrameBuffers.allocate(frame, cfg.rank)
-    ms_diff = timed(lambda: W.render_band(frame, dcfg, rays, bufs=dbufs, full_opaque_image=full))
+    ms_diff = timed(lambda: W.render_band(frame, dcfg, rays, bufs=dbufs, full_opaque_image=full, ws=ws))
     blur_ms = timed(lambda: W.resolve_blur(full, 4))
     P, n = frame.npix, frame.nfrag
     S = 1 << (cfg.rank + 1)

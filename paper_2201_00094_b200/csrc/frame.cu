@@ -47,6 +47,9 @@
 #ifndef WOIT_FLAG_INSTANCES  // general-kernel instances specialised for fixed flag sets
 #define WOIT_FLAG_INSTANCES 1
 #endif
+#ifndef WOIT_GEN_ALIASZ  // fused general kernel: z over the staged depth (as the fast path)
+#define WOIT_GEN_ALIASZ 1
+#endif
 #ifndef WOIT_GEN_DYN  // dynamic window claims in the general kernel
 #define WOIT_GEN_DYN 1
 #endif
@@ -455,7 +458,7 @@ WOIT_D void eval_chunk_fast(const zfix_t* __restrict__ zf, const float* __restri
 // and the composite with acc = wgt = 0, v_tot = 1, offset 0, D = 0, i.e. the
 // background itself -- without staging, chunks or the per-(pixel, channel) phases.
 template <int R, bool GEN>
-WOIT_D void empty_run(const KParams& kp, int flags, int64_t p0, int ne, int lane) {
+WOIT_D void empty_run(const KParams& kp, int flags, int64_t p0, int ne, int lane, const float* self = nullptr) {
     constexpr int V = 3 * (2 << R);
     if (kp.b.coeffs) {
         float* c = kp.b.coeffs + p0 * V;
@@ -505,14 +508,15 @@ WOIT_D void empty_run(const KParams& kp, int flags, int64_t p0, int ne, int lane
         if (direct) {
             const bool full = GEN && gather && kp.b.full_opaque_image;
             const float* img = full ? kp.b.full_opaque_image + (kp.f.pixel_base + p) * 3 : kp.f.opaque_color + p * 3;
-            const float r = img[0], g = img[1], b = img[2];
+            const float r = self ? self[0] : img[0], g = self ? self[1] : img[1], b = self ? self[2] : img[2];
             kp.b.output[p * 3] = r;
             kp.b.output[p * 3 + 1] = g;
             kp.b.output[p * 3 + 2] = b;
         } else {
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch)
-                kp.b.output[p * 3 + ch] = composite_channel(kp, flags, p, ch, 0.0, 0.0, 0.0, 0.0, 1.0, 0.0);
+                kp.b.output[p * 3 + ch] =
+                    composite_channel(kp, flags, p, ch, 0.0, 0.0, 0.0, 0.0, 1.0, 0.0, self ? self + ch : nullptr);
         }
     }
 }
@@ -593,7 +597,10 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
     // FL != 0: an instance specialised for exactly these flags (all but NORMALIZE)
     // (the fast path's FL is WOIT_PACKED_STORAGE for its packed-storage instance, else 0)
     const int flags = GEN ? (FL ? (FL | (kp.p.flags & WOIT_NORMALIZE)) : kp.p.flags) : ((kp.p.flags & WOIT_NORMALIZE) | FL);
-    const WLayout L = make_wlayout<R>(ph, flags, !GEN && WOIT_ALIASZ);
+    // z in place of the staged depth: the fast path, and the fused general kernel (whose
+    // refraction then reads the fragment's depth from global memory, next to its normal)
+    constexpr bool kAliasZ = WOIT_ALIASZ && (!GEN || (FUS && WOIT_GEN_ALIASZ));
+    const WLayout L = make_wlayout<R>(ph, flags, kAliasZ, GEN);
     const int lane = threadIdx.x & 31;
     WSmem<R, GEN> sm = wcarve<R, GEN>(smem_raw + (threadIdx.x >> 5) * L.total, L);
 
@@ -607,7 +614,10 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
     if (win >= nwin) return;  // warp-uniform
     // The claims are pipelined one window deep: the atomic for the window after next
     // is issued while the next window's id (claimed one window earlier) is consumed,
-    // so its round trip is hidden behind a window of work.
+    // so its round trip is hidden behind a window of work. (Deeper -- two claims in
+    // flight, or runs of 2-8 windows per claim -- measured slower on config 3: the
+    // frame ends on its heaviest windows, and every window held ahead lengthens that
+    // tail.)
     // (Fast kernel only: in the general kernel it measured slower -- the extra live
     // register spills in the generic instance, costs occupancy in the specialised ones.)
 #if WOIT_DYN
@@ -633,6 +643,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
 
     const bool do_at = ph & (PH_BUILD | PH_EVAL);
     const bool do_eval = ph & PH_EVAL;
+    const bool refr_pf = GEN && (flags & WOIT_REFRACTION);
     const bool need_coef = ph & (PH_EVAL | PH_COMPOSITE);
     const bool refr = GEN && do_eval && (flags & WOIT_REFRACTION);
     const bool diffuse = GEN && (flags & WOIT_DIFFUSION);
@@ -648,10 +659,29 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
     if (lane == 0) mbar_init(sm.bar, 1);
     uint32_t parity = 0;
     int64_t off_lane = 0, off_last;  // this window's offsets[lane] and offsets[end]
+    // General fused kernel: lane l's pixel of the next window -- its own background
+    // value (what an empty or unrefracted pixel composites over: the full image's
+    // pixel when refraction / aberration gather from it, else its opaque colour) and
+    // its opaque depth -- is prefetched into registers with the window's offsets, so
+    // empty pixels and the refraction setup do not wait on those loads.
+    constexpr bool kPF = GEN && FUS;
+    const float* bgimg = ((flags & (WOIT_CHROMATIC_ABERRATION | WOIT_REFRACTION)) && kp.b.full_opaque_image)
+                             ? kp.b.full_opaque_image + kp.f.pixel_base * 3 : kp.f.opaque_color;
+    float pf_bg[3] = {0.0f, 0.0f, 0.0f}, pf_od = INFINITY;
+    auto prefetch_px = [&](int64_t px0, int64_t pend) {
+        if (kPF && px0 + lane < pend) {
+            const int64_t pp = px0 + lane;
+            pf_bg[0] = bgimg[pp * 3];
+            pf_bg[1] = bgimg[pp * 3 + 1];
+            pf_bg[2] = bgimg[pp * 3 + 2];
+            if (refr_pf && kp.f.opaque_depth) pf_od = kp.f.opaque_depth[pp];
+        }
+    };
     {
         const int64_t end = (win * WIN + WIN) < kp.f.npix ? (win * WIN + WIN) : kp.f.npix;
         if (win * WIN + lane < end) off_lane = kp.f.offsets[win * WIN + lane];
         off_last = kp.f.offsets[end];
+        prefetch_px(win * WIN, end);
     }
     // Fast path: a sub-tile's composite (phase 7) is deferred until the next
     // sub-tile's staging copies are in flight, so it hides part of their latency.
@@ -711,7 +741,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
             const int si = sh4 + fr;
             int c0;
             float t;
-            eval_cell(sm.zfix[fr], R, c0, t);
+            eval_cell(sm.zfix[(kAliasZ ? sh4 : 0) + fr], R, c0, t);
             const float al = sm.alpha[si];
             bool cb_ = false;
             float io = 1.0f;
@@ -742,7 +772,8 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
                 const float nrm[3] = {sm.normal[3 * si], sm.normal[3 * si + 1], sm.normal[3 * si + 2]};
 #endif
                 double off[2];
-                refraction_offset(kp, d, topq, sm.depth[si], nrm, io, off);
+                // (with z over the staged depth, the depth comes from global memory)
+                refraction_offset(kp, d, topq, kAliasZ ? kp.f.depth[fa_ + fr] : sm.depth[si], nrm, io, off);
                 ro[0] += off[0];
                 ro[1] += off[1];
             }
@@ -759,6 +790,8 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
     if (off_last - wbase > (int64_t)0x7fffffff) __trap();
     if (lane < nq) sm.offs[lane] = (int32_t)(off_lane - wbase);
     if (lane == 0) sm.offs[nq] = (int32_t)(off_last - wbase);
+    // this window's prefetched per-pixel values (lane l: pixel w0 + l)
+    const float cur_bg0 = pf_bg[0], cur_bg1 = pf_bg[1], cur_bg2 = pf_bg[2], cur_od = pf_od;
     {   // prefetch the next window's offsets (consumed one window later)
         const int64_t nw = claim();
         next_win = nw;
@@ -767,8 +800,15 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
             const int64_t nend = (nw0 + WIN) < kp.f.npix ? (nw0 + WIN) : kp.f.npix;
             if (nw0 + lane < nend) off_lane = kp.f.offsets[nw0 + lane];
             off_last = kp.f.offsets[nend];
+            prefetch_px(nw0, nend);
         }
     }
+    // pixel q's prefetched values (all lanes take part in the shuffles)
+    auto self_bg = [&](int q, float out[3]) {
+        out[0] = __shfl_sync(0xffffffffu, cur_bg0, q & 31);
+        out[1] = __shfl_sync(0xffffffffu, cur_bg1, q & 31);
+        out[2] = __shfl_sync(0xffffffffu, cur_bg2, q & 31);
+    };
     __syncwarp();
     // chunks per pixel, window prefix (warp scan) and combine rotation
     int my_nch = 0;
@@ -799,7 +839,9 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
             const unsigned em = __ballot_sync(0xffffffffu, emp);
             const int ne = em == 0xffffffffu ? 32 : __ffs(~em) - 1;
             if (ne > 0) {
-                empty_run<R, GEN>(kp, flags, w0 + q0, ne, lane);
+                float sb[3];
+                if (kPF) self_bg(q0 + lane, sb);
+                empty_run<R, GEN>(kp, flags, w0 + q0, ne, lane, kPF ? sb : nullptr);
                 q0 += ne;
                 continue;
             }
@@ -932,6 +974,12 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
             // staircase v in place, read back by its own evaluation.
             const bool act = lane < nqs;
             const int64_t p = w0 + q0 + lane;
+            float tsb[3];
+            float tod = INFINITY;
+            if (kPF) {
+                self_bg(q0 + lane, tsb);
+                tod = __shfl_sync(0xffffffffu, cur_od, (q0 + lane) & 31);
+            }
             int cst = 0, clen = 0, crot = 0;
             if (act) {
                 const int oq = sm.offs[q0 + lane];
@@ -970,7 +1018,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
                 for (int j = 0; j < clen; ++j) {
                     const int fr = cst + jj;
                     jj = jj + 1 == clen ? 0 : jj + 1;
-                    sm.zfix[fr] = z_fixed_of(sm.depth[sh4 + fr], m);
+                    sm.zfix[(kAliasZ ? sh4 : 0) + fr] = z_fixed_of(sm.depth[sh4 + fr], m);
                 }
             }
             __syncwarp();
@@ -984,7 +1032,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
                         const int fr = cst + jj;
                         jj = jj + 1 == clen ? 0 : jj + 1;
                         const int si = sh4 + fr;
-                        const zfix_t zi = sm.zfix[fr];
+                        const zfix_t zi = sm.zfix[(kAliasZ ? sh4 : 0) + fr];
                         const float al = sm.alpha[si];
                         bool cb_ = false;
                         if (cube) cb_ = sm.ior[si] > 1.0f && (!bfonly || sm.bf[shb + fr] != 0);
@@ -1026,7 +1074,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
                     double d[3] = {0.0, 0.0, 0.0}, topq = INFINITY;
                     if (refr) {
                         ray_dir(kp, kp.f.pixel_base + p, d);
-                        topq = kp.f.opaque_depth ? (double)kp.f.opaque_depth[p] : INFINITY;
+                        topq = kPF ? (double)tod : kp.f.opaque_depth ? (double)kp.f.opaque_depth[p] : INFINITY;
                     }
                     eval_gen(col, cst, clen, crot, d, topq, ac, wg, df, ro);
                 }
@@ -1069,7 +1117,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
                     if (kp.b.weight) kp.b.weight[p * 3 + ch] = (float)wgt;
                     if (kp.b.output)
                         kp.b.output[p * 3 + ch] =
-                            GEN ? composite_channel(kp, flags, p, ch, acc, wgt, ro0, ro1, vt[ch], dp)
+                            GEN ? composite_channel(kp, flags, p, ch, acc, wgt, ro0, ro1, vt[ch], dp, kPF ? tsb + ch : nullptr)
                                 : composite_fast_ch(flags, acc, wgt, (double)kp.f.opaque_color[p * 3 + ch], vt[ch]);
                 }
             }
@@ -1195,7 +1243,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
                 ff = ord2f(f_);
                 if ((ph & PH_BOUNDS) && kp.b.near) kp.b.near[p] = nf;
                 if ((ph & PH_BOUNDS) && kp.b.far) kp.b.far[p] = ff;
-                if (GEN) {
+                if (GEN && !kAliasZ) {
                     const DepthMap m = depth_map(nf, ff, R);
                     sm.lo[lane] = m.lo;
                     sm.den[lane] = m.den;
@@ -1206,7 +1254,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
         // fast path: every chunk lane derives its pixel's depth map itself (the same
         // warp instructions as the pixel lanes computing it, no shared-memory round trip)
         DepthMap mq{0.0, 0.0, 0.0, 0.0};
-        if (!GEN) {
+        if (!GEN || kAliasZ) {
             const float cnf = __shfl_sync(kAll, nf, cq), cff = __shfl_sync(kAll, ff, cq);
             if (lane < C) mq = depth_map(cnf, cff, R);
         } else {
@@ -1217,14 +1265,14 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
         float* part = sm.part;
         const bool fused_z = !GEN && (ph & PH_BUILD);  // the fast build computes z itself
         if (lane < C && do_at && !fused_z) {
-            const DepthMap m{sm.lo[cq], sm.den[cq], 0.0, sm.rcp[cq]};
+            const DepthMap m = kAliasZ ? mq : DepthMap{sm.lo[cq], sm.den[cq], 0.0, sm.rcp[cq]};
 #pragma unroll kZUnroll
             for (int j = 0; j < CH; ++j) {  // independent chains: unrolled for ILP
                 if (j < clen) {
                     int jj = crot + j;
                     jj = jj >= clen ? jj - clen : jj;
                     const int fr = cst + jj;
-                    sm.zfix[fr] = z_fixed_of(sm.depth[sh4 + fr], m);
+                    sm.zfix[(kAliasZ ? sh4 : 0) + fr] = z_fixed_of(sm.depth[sh4 + fr], m);
                 }
             }
         }
@@ -1252,7 +1300,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
                     const int fr = cst + jj;   // fragment index relative to fa
                     jj = jj + 1 == clen ? 0 : jj + 1;
                     const int si = sh4 + fr;   // staging index
-                    const zfix_t zi = sm.zfix[fr];
+                    const zfix_t zi = sm.zfix[(kAliasZ ? sh4 : 0) + fr];
                     const float al = sm.alpha[si];
                     bool cb_ = false;
                     if (cube) cb_ = sm.ior[si] > 1.0f && (!bfonly || sm.bf[shb + fr] != 0);
@@ -1503,6 +1551,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
 
         // ---- 6. evaluate (step3): v̂ per fragment, chunk accumulators --------------
         if (do_eval) {
+            const float cod = kPF ? __shfl_sync(0xffffffffu, cur_od, (q0 + cq) & 31) : INFINITY;
             if (lane < C) {
                 const float2* cq2 = sm.cells + cq * CellRow<M>::CR;
                 float ac[3] = {0.f, 0.f, 0.f}, wg[3] = {0.f, 0.f, 0.f}, df = 0.f;
@@ -1511,7 +1560,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
                 const int64_t p = w0 + q0 + cq;
                 if (refr) {
                     ray_dir(kp, kp.f.pixel_base + p, d);
-                    topq = kp.f.opaque_depth ? (double)kp.f.opaque_depth[p] : INFINITY;
+                    topq = kPF ? (double)cod : kp.f.opaque_depth ? (double)kp.f.opaque_depth[p] : INFINITY;
                 }
                 const bool op_staged = ph & PH_BUILD;  // the build left alpha (1 - T') in the trans slot
                 if (!GEN) {
@@ -1528,7 +1577,7 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
                     sm.accp[6 * AR + lane] = (float)ro[0];
                     sm.accp[7 * AR + lane] = (float)ro[1];
                 }
-                if (GEN) sm.accp[8 * AR + lane] = df;
+                if (diffuse) sm.accp[8 * AR + lane] = df;  // (the row exists with diffusion only)
             }
             fence_proxy_async();  // v̂ in smem becomes visible to the bulk store
             __syncwarp();
@@ -1555,6 +1604,13 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
         }
 
         // ---- 7. per-pixel accumulators + composite (step4) -------------------------
+        float csb = 0.0f;  // lane (pixel kq, channel kch)'s prefetched background value
+        if (kPF) {
+            const int kch = lane / nqs, kq = lane - kch * nqs;
+            float b[3];
+            self_bg(q0 + kq, b);
+            csb = kch == 0 ? b[0] : kch == 1 ? b[1] : b[2];
+        }
         if (!GEN) {
             // fast path: deferred to the next sub-tile's staging (composite_fast)
             pend = true;
@@ -1604,7 +1660,8 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
                 }
             }
             if ((ph & PH_COMPOSITE) && kp.b.output)
-                kp.b.output[p * 3 + kch] = composite_channel(kp, flags, p, kch, acc, wgt, ro0, ro1, (double)sm.vtot[kq * 3 + kch], dp);
+                kp.b.output[p * 3 + kch] = composite_channel(kp, flags, p, kch, acc, wgt, ro0, ro1,
+                                                             (double)sm.vtot[kq * 3 + kch], dp, kPF ? &csb : nullptr);
         }
         fence_proxy_async();
         __syncwarp();
@@ -1887,7 +1944,8 @@ template <int R, bool GEN, bool FUS, int VAR, int FL = 0>
 cudaError_t launch_tiles(const KParams& kp, cudaStream_t st) {
     using G = WT<R>;
     const uint32_t ph = (GEN && !FUS) ? kp.phases : (PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE);
-    const WLayout L = make_wlayout<R>(ph, GEN ? kp.p.flags : ((kp.p.flags & WOIT_NORMALIZE) | FL), !GEN && WOIT_ALIASZ);
+    constexpr bool kAliasZ = WOIT_ALIASZ && (!GEN || (FUS && WOIT_GEN_ALIASZ));  // as frame_kernel
+    const WLayout L = make_wlayout<R>(ph, GEN ? kp.p.flags : ((kp.p.flags & WOIT_NORMALIZE) | FL), kAliasZ, GEN);
     const int bytes = (int)(L.total * G::WPB);
     // persistent grid: as many CTAs as can be resident, each warp loops over windows
     const int64_t warps = (kp.f.npix + G::WIN - 1) / G::WIN;

@@ -89,7 +89,7 @@ struct PartRows {
 // and nothing reads the depth afterwards), every chunk lane derives its own depth map
 // (no per-pixel map arrays), and exp(-A_total) lives in the reused partials region.
 template <int R>
-WOIT_HD WLayout make_wlayout(uint32_t phases, int flags, bool alias_z) {
+WOIT_HD WLayout make_wlayout(uint32_t phases, int flags, bool alias_z, bool gen) {
     using G = WT<R>;
     const bool at = phases & (PH_BUILD | PH_EVAL);
     const bool ev = phases & PH_EVAL;
@@ -125,7 +125,10 @@ WOIT_HD WLayout make_wlayout(uint32_t phases, int flags, bool alias_z) {
     const bool tight = phases == (PH_BOUNDS | PH_BUILD | PH_EVAL | PH_COMPOSITE);  // the fused render's own bounds
     const uint32_t part_b = (phases & PH_BUILD) ? 4u * 3 * 32 * PartRows<R>::n(tight) : 0u;
     const uint32_t cells_b = (uint32_t)G::SUBP * (G::S + 1) * 24u;  // frame.cu CellTab
-    const uint32_t acc_b = ev ? align16(4u * (alias_z ? 6 : 9) * 33) : 0u;  // rows of 33 (frame.cu AR)
+    // chunk accumulators: acc / weight (6 rows), + refraction offset (2) and diffusion
+    // coverage (1) in the general kernel; rows of 33 (frame.cu AR)
+    const uint32_t acc_rows = !gen ? 6u : (flags & WOIT_DIFFUSION) ? 9u : 8u;
+    const uint32_t acc_b = ev ? align16(4u * acc_rows * 33) : 0u;
     const uint32_t vtot_b = alias_z ? align16(4u * 3 * G::SUBP) : 0u;
     const uint32_t words_b = packed ? align16(4u * G::SUBP * G::S) : 0u;  // E5B9G9R9 words of the sub-tile
     const uint32_t after_b = align16(4u * G::SUBP * G::V) + align16(cells_b) + acc_b + vtot_b + words_b;
@@ -135,7 +138,7 @@ WOIT_HD WLayout make_wlayout(uint32_t phases, int flags, bool alias_z) {
     L.accp = L.cells + align16(cells_b);
     if (alias_z) L.vtot = L.accp + acc_b;
     L.words = L.accp + acc_b + vtot_b;
-    L.opq = o;   o = align16(o + 12u * (G::SUBP + 4));  // [pa & ~3, pb rounded up to 4)
+    L.opq = o;   o = align16(o + (gen ? 0u : 12u * (G::SUBP + 4)));  // fast path: [pa & ~3, pb rounded up to 4)
     L.bar = o;   o = align16(o + 16u);
 #ifdef WOIT_SMEM_PAD
     o += WOIT_SMEM_PAD;
@@ -184,6 +187,19 @@ WOIT_HD void spectral_weight(int i, int k, bool literal, double w[3]) {
     w[1] = g - wb;
     w[2] = wb;
 #endif
+}
+
+// column / row of global pixel gp in an image W wide: 32-bit division when the id
+// fits (every image the ABI accepts: width * height < 2^31), 64-bit otherwise
+WOIT_D void pixel_xy(int64_t gp, int W, double& px, double& py) {
+    if ((uint64_t)gp <= 0xffffffffull) {
+        const uint32_t g = (uint32_t)gp, w = (uint32_t)W, y = g / w;
+        px = (double)(g - y * w);
+        py = (double)y;
+    } else {
+        px = (double)(gp % W);
+        py = (double)(gp / W);
+    }
 }
 
 // bilinear_sample (pipeline.py:242-255): edge clamped, in f64
@@ -235,14 +251,15 @@ WOIT_D void tap(const TapTable& tt, int i, int k, bool lit, double& fac, double 
 }
 
 // Channel `ch` of the background of one pixel (pipeline.py:290-303); see sample_background.
+// `self`, when not null, holds img[gp * 3 + ch] already loaded (a register prefetch).
 WOIT_D double sample_background_ch(const float* img, int W, int H, int64_t gp, int flags, int taps,
-                                   const TapTable& tt, double ox, double oy, int ch) {
+                                   const TapTable& tt, double ox, double oy, int ch,
+                                   const float* self = nullptr) {
     if (flags & (WOIT_CHROMATIC_ABERRATION | WOIT_REFRACTION)) {
-        const double px = (double)(gp % W), py = (double)(gp / W);
         if (ox == 0.0 && oy == 0.0) {
             // every tap lands on the pixel itself, where the bilinear weights are exactly
             // (1, 0) and the sample is exactly the pixel: same arithmetic, no gathers
-            const double s0 = (double)img[gp * 3 + ch];
+            const double s0 = self ? (double)*self : (double)img[gp * 3 + ch];
             // with 0/1 weights (k = 3, 5, 7) the sum is m s0 exactly (s0 is fp32-valued)
             // and m s0 / m == s0: the pixel itself, bit for bit
             if (!(flags & WOIT_CHROMATIC_ABERRATION) || (tt.n == taps && tt.unit)) return s0;
@@ -256,6 +273,8 @@ WOIT_D double sample_background_ch(const float* img, int W, int H, int64_t gp, i
             }
             return den > 0.0 ? ddiv(num, den) : s0;
         }
+        double px, py;
+        pixel_xy(gp, W, px, py);
         if (flags & WOIT_CHROMATIC_ABERRATION) {
             const bool lit = flags & WOIT_LITERAL_SPECTRAL_T;
             double num = 0.0, den = 0.0;
@@ -271,7 +290,7 @@ WOIT_D double sample_background_ch(const float* img, int W, int H, int64_t gp, i
         }
         return bilinear_ch(img, W, H, dadd(px, ox), dadd(py, oy), ch);
     }
-    return (double)img[gp * 3 + ch];
+    return self ? (double)*self : (double)img[gp * 3 + ch];
 }
 
 // Background of one pixel read from `img` (pipeline.py:290-303): the k-tap aberration
@@ -280,7 +299,8 @@ WOIT_D double sample_background_ch(const float* img, int W, int H, int64_t gp, i
 WOIT_D void sample_background(const float* img, int W, int H, int64_t gp, int flags, int taps,
                               const TapTable& tt, double ox, double oy, double bg[3]) {
     if (flags & (WOIT_CHROMATIC_ABERRATION | WOIT_REFRACTION)) {
-        const double px = (double)(gp % W), py = (double)(gp / W);
+        double px, py;
+        pixel_xy(gp, W, px, py);
         if (ox == 0.0 && oy == 0.0 && (!(flags & WOIT_CHROMATIC_ABERRATION) || (tt.n == taps && tt.unit))) {
             // exact bilinear weights (1, 0) at the pixel, 0/1 tap weights: the pixel itself
 #pragma unroll
@@ -375,9 +395,10 @@ WOIT_D void composite_plain(int flags, const float bgc[3], const double acc[3], 
 }
 
 // Channel `ch` of composite_pixel, for per-(pixel, channel) lanes: the same
-// operations, so the result is bit-identical to composite_pixel's channel.
+// operations, so the result is bit-identical to composite_pixel's channel. `self`:
+// as in sample_background_ch (the pixel's own background value, prefetched), or null.
 WOIT_D float composite_channel(const KParams& kp, int flags, int64_t p, int ch, double acc, double wgt, double ox,
-                               double oy, double vt, double dp) {
+                               double oy, double vt, double dp, const float* self = nullptr) {
     const int W = kp.f.width;
     // flags as in composite_pixel
     const bool gather = flags & (WOIT_CHROMATIC_ABERRATION | WOIT_REFRACTION);
@@ -385,8 +406,8 @@ WOIT_D float composite_channel(const KParams& kp, int flags, int64_t p, int ch, 
     const int H = full ? kp.f.height : (int)(kp.f.npix / W);
     const int64_t gp = full ? kp.f.pixel_base + p : p;
     double bg = gather ? sample_background_ch(full ? kp.b.full_opaque_image : kp.f.opaque_color, W, H, gp,
-                                              flags, kp.p.aberration_taps, kp.taps, ox, oy, ch)
-                       : (double)kp.f.opaque_color[p * 3 + ch];
+                                              flags, kp.p.aberration_taps, kp.taps, ox, oy, ch, self)
+                       : (self ? (double)*self : (double)kp.f.opaque_color[p * 3 + ch]);
     if (flags & WOIT_DIFFUSION) {
         const double bb = sample_background_ch(kp.b.blurred_image, W, H, gp, flags, kp.p.aberration_taps,
                                                kp.taps, ox, oy, ch);
@@ -402,7 +423,8 @@ WOIT_D float composite_channel(const KParams& kp, int flags, int64_t p, int ch, 
 // Primary ray direction of global pixel gp (scene.py:199-212), f64.
 WOIT_D void ray_dir(const KParams& kp, int64_t gp, double d[3]) {
     const int W = kp.f.width, H = kp.f.height;
-    const double px = (double)(gp % W), py = (double)(gp / W);
+    double px, py;
+    pixel_xy(gp, W, px, py);
     const double u = dmul(dmul(dsub(ddiv(dmul(2.0, dadd(px, 0.5)), (double)W), 1.0), kp.p.tan_half),
                           kp.p.aspect);
     const double v = dmul(dsub(1.0, ddiv(dmul(2.0, dadd(py, 0.5)), (double)H)), kp.p.tan_half);

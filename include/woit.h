@@ -303,9 +303,10 @@ int woit_bin_by_pixel(const int64_t* pix, int64_t n, int64_t npix, int64_t* offs
                       int64_t* perm, void* ws, size_t ws_bytes, void* stream);
 
 /* An unbinned stream -> the CSR stream the frame kernels take (scene.py:559-566): the
- * same stable sort, with the last pass scattering every fragment's fields (depth,
- * alpha, trans, radiance, normal, ior, backface -- each present on both sides or
- * neither) straight from its arrival slot into its CSR slot. unbinned->nfrag / npix
+ * same stable sort, then every fragment's fields (depth, alpha, trans, radiance,
+ * normal, ior, backface -- each present on both sides or neither) move from its
+ * arrival slot into its CSR slot, 32 pixels at a time (reads coalesce when the
+ * arrival is layer by layer). unbinned->nfrag / npix
  * give the sizes (unbinned->offsets unused); binned's field pointers are the outputs
  * (its const qualifiers notwithstanding); offsets int64[npix+1]; perm int64[n] or NULL. */
 size_t woit_bin_frame_workspace_bytes(int64_t n, int64_t npix);

@@ -11,15 +11,18 @@
 //   scan       per digit, the exclusive scan of its counts over the tiles (one CTA
 //              per digit, contiguous rows), plus the digit totals;
 //   scatter    per tile: stable local ranks -- each warp walks its 512 ids in
-//              rounds of 32 consecutive ids, __match_any_sync groups a round's equal
+//              rounds of 32 consecutive ids, eight ballots group a round's equal
 //              digits (rank = lanes before in the group + the warp's running count),
 //              warps are ordered by a per-digit scan over the warps -- then the tile
 //              is reordered in shared memory and written out as one contiguous run
-//              per digit (coalesced). The last pass writes perm and, fused, gathers
-//              each fragment's fields from its original index into its CSR slot
-//              (a separate full-occupancy gather kernel after the sort measured 0.9 ms
-//              slower at config 2: its reads, 32 scattered sectors per warp load,
-//              multiply L2 traffic; the fused pass issues all of a thread's loads first).
+//              per digit (coalesced). The last pass writes perm.
+// The fields of bin_frame then move in CSR order by gather_kernel: a tile of 32
+// pixels at a time, lanes = pixels and warps = each pixel's k-th fragments, so a warp
+// load reads the k-th fragments of 32 consecutive pixels -- consecutive arrival slots
+// when the producer emits the frame layer by layer -- and the tile leaves through
+// shared memory as contiguous runs. (It replaced a gather fused into the last pass,
+// whose reads from the arrival slots of pixel-sorted ids scattered over 32 sectors
+// per warp load: 4 ms of the 6.1 ms at config 2.)
 // Bit-exact to the reference's numpy binning (tests/test_gpu_parity.py).
 #include "common.cuh"
 #include "internal.cuh"
@@ -149,22 +152,25 @@ __global__ void __launch_bounds__(1024) scan_rows_kernel(int32_t* __restrict__ c
 }
 
 struct Gather {
-    // fused field gather of the last pass (null `in.depth`: none)
+    // fields moved into CSR order after the sort (null `in.depth`: none)
     woit_frags_t in;
     woit_frags_t out;
     int64_t* perm;  // argsort(pix, stable); may be null
 };
 
-// one stable counting-sort pass over digit (key >> shift) & 255; GATHER (last pass
-// only) scatters the fragment fields instead of the ids
-template <typename K, bool FIRST, bool LAST, bool GATHER>
-__global__ void __launch_bounds__(kThreads, GATHER ? 1 : 4) scatter_kernel(const K* __restrict__ keys_in,
-                                                           const int32_t* __restrict__ vals_in, int64_t n,
-                                                           int shift, int64_t tiles,
-                                                           const int32_t* __restrict__ counts,
-                                                           const int32_t* __restrict__ totals,
-                                                           int32_t* __restrict__ keys_out,
-                                                           int32_t* __restrict__ vals_out, const Gather g) {
+// one stable counting-sort pass over digit (key >> shift) & 255; the last pass writes
+// perm (int64, if asked) and, for the field gather, the int32 ids (`vals_out` non-null)
+#ifndef WOIT_BIN_MINB
+#define WOIT_BIN_MINB 4
+#endif
+template <typename K, bool FIRST, bool LAST>
+__global__ void __launch_bounds__(kThreads, WOIT_BIN_MINB) scatter_kernel(const K* __restrict__ keys_in,
+                                                              const int32_t* __restrict__ vals_in, int64_t n,
+                                                              int shift, int64_t tiles,
+                                                              const int32_t* __restrict__ counts,
+                                                              const int32_t* __restrict__ totals,
+                                                              int32_t* __restrict__ keys_out,
+                                                              int32_t* __restrict__ vals_out, const Gather g) {
     __shared__ int warp_cnt[kWarps][kRadix];  // running, then per-warp base of each digit
     __shared__ int tile_start[kRadix];        // digit's first slot in the reordered tile
     __shared__ int gbase[kRadix];             // digit's first global slot for this tile
@@ -193,25 +199,40 @@ __global__ void __launch_bounds__(kThreads, GATHER ? 1 : 4) scatter_kernel(const
         gbase[d] = before + x - v + counts[(int64_t)d * tiles + t];
     }
     __syncthreads();
-    // stable ranks within the warp's 512 consecutive ids, rounds of 32
+    // stable ranks within the warp's 512 consecutive ids, rounds of 32; every key and
+    // id is loaded first (the rounds' __syncwarp would otherwise serialise the loads)
     int kk[kPerThread], vv[kPerThread], rk[kPerThread];
 #pragma unroll
     for (int r = 0; r < kPerThread; ++r) {
         const int le = w * (kPerThread * 32) + r * 32 + lane;  // tile-local element
-        const bool act = le < tn;
         const int64_t e = base + le;
-        const int key = act ? key_at(keys_in, e) : 0;
-        const int val = act ? (FIRST ? (int)e : vals_in[e]) : 0;
+        kk[r] = le < tn ? key_at(keys_in, e) : 0;
+        vv[r] = le < tn ? (FIRST ? (int)e : vals_in[e]) : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < kPerThread; ++r) {
+        const int le = w * (kPerThread * 32) + r * 32 + lane;  // tile-local element
+        const bool act = le < tn;
+        const int key = kk[r];
         const int d = act ? (key >> shift) & (kRadix - 1) : kRadix;  // inactive lanes: their own group
-        const unsigned grp = __match_any_sync(0xffffffffu, d);
+        // lanes with the same digit: one ballot per digit bit (a warp multisplit; the
+        // hardware match instruction measured 35% of this kernel's stalls)
+        unsigned grp = __ballot_sync(0xffffffffu, act);
+        grp = act ? grp : ~grp;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const bool bit = (d >> b) & 1;
+            const unsigned m = __ballot_sync(0xffffffffu, bit);
+            grp &= bit ? m : ~m;
+        }
         const int before = __popc(grp & ((1u << lane) - 1u));
+        // the group's leader advances the warp's running count of the digit (shared
+        // atomics of one warp to one address apply in program order, so the rounds
+        // need no barrier between them) and hands the old count to its group
+        const int leader = __ffs(grp) - 1;
         int run = 0;
-        if (act) run = warp_cnt[w][d];
-        __syncwarp();
-        if (act && before == 0) warp_cnt[w][d] = run + __popc(grp);
-        __syncwarp();
-        kk[r] = key;
-        vv[r] = val;
+        if (act && before == 0) run = atomicAdd(&warp_cnt[w][d], __popc(grp));
+        run = __shfl_sync(0xffffffffu, run, leader);
         rk[r] = act ? run + before : -1;
     }
     __syncthreads();
@@ -249,62 +270,13 @@ __global__ void __launch_bounds__(kThreads, GATHER ? 1 : 4) scatter_kernel(const
     }
     __syncthreads();
     // out: one contiguous run per digit
-    if (!GATHER) {
-        for (int i = threadIdx.x; i < tn; i += kThreads) {
-            const int key = skey[i], val = sval[i];
-            const int d = (key >> shift) & (kRadix - 1);
-            const int64_t gp = (int64_t)gbase[d] + (i - tile_start[d]);
-            keys_out[gp] = key;
-            if (!LAST) vals_out[gp] = val;
-            if (LAST && g.perm) g.perm[gp] = val;
-        }
-    } else {
-        // last pass with the fused gather: every fragment's fields from its arrival slot
-        // into its CSR slot. The reads are random, so each thread first issues the
-        // loads of all its fragments (memory-level parallelism), then stores them.
-        const woit_frags_t a = g.in, b = g.out;
-        constexpr int kG = kPerThread;
-        float dep[kG], alp[kG], tr[kG][3], ra[kG][3];
-        int64_t gps[kG];
-        int vals[kG];
-#pragma unroll
-        for (int j = 0; j < kG; ++j) {
-            const int i = threadIdx.x + j * kThreads;
-            gps[j] = -1;
-            if (i < tn) {
-                const int key = skey[i], val = sval[i];
-                const int d = (key >> shift) & (kRadix - 1);
-                gps[j] = (int64_t)gbase[d] + (i - tile_start[d]);
-                vals[j] = val;
-                keys_out[gps[j]] = key;
-                const int64_t v = val;
-                dep[j] = __ldg(a.depth + v);
-                alp[j] = a.alpha ? __ldg(a.alpha + v) : 0.0f;
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    tr[j][c] = a.trans ? __ldg(a.trans + 3 * v + c) : 0.0f;
-                    ra[j][c] = a.radiance ? __ldg(a.radiance + 3 * v + c) : 0.0f;
-                }
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < kG; ++j) {
-            if (gps[j] < 0) continue;
-            const int64_t gp = gps[j], v = vals[j];
-            if (g.perm) g.perm[gp] = v;
-            const_cast<float*>(b.depth)[gp] = dep[j];
-            if (a.alpha) const_cast<float*>(b.alpha)[gp] = alp[j];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                if (a.trans) const_cast<float*>(b.trans)[3 * gp + c] = tr[j][c];
-                if (a.radiance) const_cast<float*>(b.radiance)[3 * gp + c] = ra[j][c];
-            }
-            if (a.normal)
-#pragma unroll
-                for (int c = 0; c < 3; ++c) const_cast<float*>(b.normal)[3 * gp + c] = __ldg(a.normal + 3 * v + c);
-            if (a.ior) const_cast<float*>(b.ior)[gp] = __ldg(a.ior + v);
-            if (a.backface) const_cast<uint8_t*>(b.backface)[gp] = __ldg(a.backface + v);
-        }
+    for (int i = threadIdx.x; i < tn; i += kThreads) {
+        const int key = skey[i], val = sval[i];
+        const int d = (key >> shift) & (kRadix - 1);
+        const int64_t gp = (int64_t)gbase[d] + (i - tile_start[d]);
+        keys_out[gp] = key;
+        if (!LAST || vals_out) vals_out[gp] = val;
+        if (LAST && g.perm) g.perm[gp] = val;
     }
 }
 
@@ -316,6 +288,162 @@ __global__ void offsets_kernel(const int32_t* __restrict__ keys, int64_t n, int6
         const int64_t hi = i == n ? npix : (int64_t)keys[i];
         for (int64_t p = lo; p <= hi; ++p) offsets[p] = i;
     }
+}
+
+// Fields into CSR order: out[s] = in[perm[s]] for every field present. One tile of
+// kGP = 32 pixels per iteration: lane = pixel, warp w takes the pixel's fragments
+// k = kc + w, kc + w + 8, ... of the chunk [kc, kc + kGK); a thread issues all its
+// id and field loads before staging them in shared memory ([field][k][pixel], rows of
+// 33: conflict-free both ways); the chunk then leaves as each pixel's run of slots,
+// consecutive threads on consecutive slots. Tiles with a pixel deeper than kGDeep
+// copy slot by slot instead (a pixel's k-th fragments have no neighbours to share
+// sectors with).
+constexpr int kGT = 256, kGW = kGT / 32, kGP = 32, kGK = 32, kGDeep = 4096;
+constexpr int kGPlane = kGK * (kGP + 1);  // floats per staged field
+
+template <bool REFR>
+__global__ void __launch_bounds__(kGT) gather_kernel(const int64_t* __restrict__ offsets,
+                                                     const int32_t* __restrict__ perm, int64_t npix,
+                                                     const woit_frags_t in, const woit_frags_t out) {
+    extern __shared__ float gst[];  // [planes][kGK][kGP + 1] (+ backface bytes)
+    constexpr int NPL = REFR ? 12 : 8;  // depth, alpha, trans 3, radiance 3 (+ normal 3, ior)
+    uint8_t* gbf = reinterpret_cast<uint8_t*>(gst + NPL * kGPlane);
+    __shared__ int s_len[kGP + 1];      // chunk run-length prefix over the tile's pixels
+    __shared__ int64_t s_slot[kGP];     // first slot of the pixel's chunk run
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const bool has_a = in.alpha, has_t = in.trans, has_r = in.radiance;
+    const bool has_n = REFR && in.normal, has_i = REFR && in.ior, has_b = REFR && in.backface;
+    float* od = const_cast<float*>(out.depth);
+    float* oa = const_cast<float*>(out.alpha);
+    float* ot = const_cast<float*>(out.trans);
+    float* orad = const_cast<float*>(out.radiance);
+    float* on = const_cast<float*>(out.normal);
+    float* oi = const_cast<float*>(out.ior);
+    uint8_t* ob_ = const_cast<uint8_t*>(out.backface);
+    const int64_t ntile = (npix + kGP - 1) / kGP;
+    for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+        const int64_t p0 = tile * kGP;
+        const int np = (int)((npix - p0) < kGP ? (npix - p0) : kGP);
+        const int64_t o_p = offsets[p0 + (lane < np ? lane : np)];
+        const int c_p = lane < np ? (int)(offsets[p0 + lane + 1] - o_p) : 0;
+        const int cmax = __reduce_max_sync(0xffffffffu, c_p);
+        if (cmax > kGDeep) {  // slot by slot
+            const int64_t s0 = __shfl_sync(0xffffffffu, o_p, 0), s1 = offsets[p0 + np];
+            for (int64_t s = s0 + threadIdx.x; s < s1; s += kGT) {
+                const int64_t a = perm[s];
+                od[s] = in.depth[a];
+                if (has_a) oa[s] = in.alpha[a];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    if (has_t) ot[3 * s + c] = in.trans[3 * a + c];
+                    if (has_r) orad[3 * s + c] = in.radiance[3 * a + c];
+                    if (has_n) on[3 * s + c] = in.normal[3 * a + c];
+                }
+                if (has_i) oi[s] = in.ior[a];
+                if (has_b) ob_[s] = in.backface[a];
+            }
+            continue;
+        }
+        for (int kc = 0; kc < cmax; kc += kGK) {
+            // read: ids, then the fields of this thread's (pixel, k) pairs
+            constexpr int KPW = kGK / kGW;  // pairs per thread
+            int64_t a[KPW];
+#pragma unroll
+            for (int j = 0; j < KPW; ++j) {
+                const int k = kc + w + kGW * j;
+                a[j] = k < c_p ? (int64_t)perm[o_p + k] : -1;
+            }
+            float f[KPW][NPL];
+            uint8_t fb[KPW];
+#pragma unroll
+            for (int j = 0; j < KPW; ++j) {
+                if (a[j] < 0) continue;
+                const int64_t x = a[j];
+                f[j][0] = __ldg(in.depth + x);
+                f[j][1] = has_a ? __ldg(in.alpha + x) : 0.0f;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    f[j][2 + c] = has_t ? __ldg(in.trans + 3 * x + c) : 0.0f;
+                    f[j][5 + c] = has_r ? __ldg(in.radiance + 3 * x + c) : 0.0f;
+                    if (REFR) f[j][8 + c] = has_n ? __ldg(in.normal + 3 * x + c) : 0.0f;
+                }
+                if (REFR) f[j][NPL - 1] = has_i ? __ldg(in.ior + x) : 0.0f;
+                fb[j] = has_b ? __ldg(in.backface + x) : 0;
+            }
+            // the chunk's run per pixel, its prefix over the tile, its first slot
+            const int len = c_p - kc < 0 ? 0 : (c_p - kc < kGK ? c_p - kc : kGK);
+            if (w == 0) {
+                int x = len;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                s_len[lane + 1] = x;
+                if (lane == 0) s_len[0] = 0;
+                s_slot[lane] = o_p + kc;
+            }
+#pragma unroll
+            for (int j = 0; j < KPW; ++j) {
+                if (a[j] < 0) continue;
+                const int r = (w + kGW * j) * (kGP + 1) + lane;
+#pragma unroll
+                for (int q = 0; q < NPL; ++q) gst[q * kGPlane + r] = f[j][q];
+                if (has_b) gbf[r] = fb[j];
+            }
+            __syncthreads();
+            // write: the runs, consecutive threads on consecutive slots
+            const int tot = s_len[kGP];
+            auto locate = [&](int i, int& q, int& kk) {  // i-th slot of the chunk -> (pixel, k)
+                q = 0;
+#pragma unroll
+                for (int st = kGP / 2; st >= 1; st >>= 1)
+                    if (s_len[q + st] <= i) q += st;
+                kk = i - s_len[q];
+            };
+            for (int i = threadIdx.x; i < tot; i += kGT) {
+                int q, kk;
+                locate(i, q, kk);
+                const int64_t s = s_slot[q] + kk;
+                const int r = kk * (kGP + 1) + q;
+                od[s] = gst[r];
+                if (has_a) oa[s] = gst[kGPlane + r];
+                if (has_i) oi[s] = gst[(NPL - 1) * kGPlane + r];
+                if (has_b) ob_[s] = gbf[r];
+            }
+            for (int i = threadIdx.x; i < 3 * tot; i += kGT) {
+                const int e = i / 3, c = i - 3 * e;
+                int q, kk;
+                locate(e, q, kk);
+                const int64_t s = s_slot[q] + kk;
+                const int r = kk * (kGP + 1) + q;
+                if (has_t) ot[3 * s + c] = gst[(2 + c) * kGPlane + r];
+                if (has_r) orad[3 * s + c] = gst[(5 + c) * kGPlane + r];
+                if (has_n) on[3 * s + c] = gst[(8 + c) * kGPlane + r];
+            }
+            __syncthreads();
+        }
+    }
+}
+
+template <bool REFR>
+constexpr size_t gather_smem() { return (REFR ? 12 : 8) * kGPlane * sizeof(float) + kGPlane; }
+
+template <bool REFR>
+cudaError_t launch_gather(const int64_t* offsets, const int32_t* perm, int64_t npix, const Gather& g,
+                          cudaStream_t st) {
+    const size_t smem = gather_smem<REFR>();
+    cudaError_t err = cudaFuncSetAttribute(gather_kernel<REFR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gather_kernel<REFR>, kGT, smem);
+    const int64_t ntile = (npix + kGP - 1) / kGP;
+    int64_t grid = (int64_t)sms * (per > 0 ? per : 1);
+    grid = grid < ntile ? grid : ntile;
+    gather_kernel<REFR><<<(unsigned)grid, kGT, smem, st>>>(offsets, perm, npix, g.in, g.out);
+    return cudaGetLastError();
 }
 
 template <typename K>
@@ -337,24 +465,21 @@ cudaError_t run(const K* pix, int64_t n, int64_t npix, int64_t* offsets, const G
         scan_rows_kernel<<<kRadix, 1024, 0, st>>>(p.counts, p.tiles, p.totals);
         int32_t* ko = p.keys[cur];
         int32_t* vo = p.vals[cur];
-        const bool gather = last && g.in.depth;
+        // the field gather needs the int32 ids of the last pass
+        int32_t* vlast = g.in.depth ? vo : nullptr;
         const dim3 gr(tiles), bl(kThreads);
         if (first && last)
-            gather ? scatter_kernel<K, true, true, true><<<gr, bl, 0, st>>>(pix, nullptr, n, shift, p.tiles, p.counts,
-                                                                              p.totals, ko, vo, g)
-                   : scatter_kernel<K, true, true, false><<<gr, bl, 0, st>>>(pix, nullptr, n, shift, p.tiles,
-                                                                               p.counts, p.totals, ko, vo, g);
+            scatter_kernel<K, true, true><<<gr, bl, 0, st>>>(pix, nullptr, n, shift, p.tiles, p.counts, p.totals, ko,
+                                                             vlast, g);
         else if (first)
-            scatter_kernel<K, true, false, false><<<gr, bl, 0, st>>>(pix, nullptr, n, shift, p.tiles, p.counts,
-                                                                       p.totals, ko, vo, g);
+            scatter_kernel<K, true, false><<<gr, bl, 0, st>>>(pix, nullptr, n, shift, p.tiles, p.counts, p.totals, ko,
+                                                              vo, g);
         else if (last)
-            gather ? scatter_kernel<int32_t, false, true, true><<<gr, bl, 0, st>>>(kin, vin, n, shift, p.tiles,
-                                                                                    p.counts, p.totals, ko, vo, g)
-                   : scatter_kernel<int32_t, false, true, false><<<gr, bl, 0, st>>>(kin, vin, n, shift, p.tiles,
-                                                                                     p.counts, p.totals, ko, vo, g);
+            scatter_kernel<int32_t, false, true><<<gr, bl, 0, st>>>(kin, vin, n, shift, p.tiles, p.counts, p.totals,
+                                                                    ko, vlast, g);
         else
-            scatter_kernel<int32_t, false, false, false><<<gr, bl, 0, st>>>(kin, vin, n, shift, p.tiles, p.counts,
-                                                                              p.totals, ko, vo, g);
+            scatter_kernel<int32_t, false, false><<<gr, bl, 0, st>>>(kin, vin, n, shift, p.tiles, p.counts, p.totals,
+                                                                     ko, vo, g);
         cudaError_t err = cudaGetLastError();
         if (err != cudaSuccess) return err;
         kin = ko;
@@ -363,7 +488,10 @@ cudaError_t run(const K* pix, int64_t n, int64_t npix, int64_t* offsets, const G
     }
     const int64_t g2 = (n + 256) / 256;
     offsets_kernel<<<(unsigned)(g2 < 8192 ? g2 : 8192), 256, 0, st>>>(kin, n, npix, offsets);
-    return cudaGetLastError();
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess || !g.in.depth) return err;
+    const bool refr = g.in.normal || g.in.ior || g.in.backface;
+    return refr ? launch_gather<true>(offsets, vin, npix, g, st) : launch_gather<false>(offsets, vin, npix, g, st);
 }
 
 }  // namespace bin

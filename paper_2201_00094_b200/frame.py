@@ -165,22 +165,29 @@ class FrameFragments:
         if pix.dtype != torch.int32 or pix.numel() != n or pix.device != dev:
             raise ValueError("pix must be an int32 device tensor with one pixel id per fragment")
         f32 = lambda t, *shape: t.to(dev, torch.float32).contiguous().reshape(*shape)
-        if normal is None:
-            normal = torch.tensor([0.0, 0.0, -1.0], device=dev).repeat(n, 1)
-        if ior is None:
-            ior = torch.ones(n, device=dev)
-        if backface is None:
-            backface = torch.zeros(n, dtype=torch.uint8, device=dev)
-        ins = dict(depth=f32(depth, n), alpha=f32(alpha, n), trans=f32(trans, n, 3), radiance=f32(radiance, n, 3),
-                   normal=f32(normal, n, 3), ior=f32(ior, n), backface=backface.to(dev, torch.uint8).contiguous())
+        ins = dict(depth=f32(depth, n), alpha=f32(alpha, n), trans=f32(trans, n, 3), radiance=f32(radiance, n, 3))
+        if normal is not None:
+            ins["normal"] = f32(normal, n, 3)
+        if ior is not None:
+            ins["ior"] = f32(ior, n)
+        if backface is not None:
+            ins["backface"] = backface.to(dev, torch.uint8).contiguous()
         outs = {k: torch.empty_like(v) for k, v in ins.items()}
+        # absent refraction fields are not moved: their CSR arrays are the constants
+        # the frame kernels take for "none" (normal (0, 0, -1), ior 1, front face)
+        if normal is None:
+            outs["normal"] = torch.tensor([0.0, 0.0, -1.0], device=dev).repeat(n, 1)
+        if ior is None:
+            outs["ior"] = torch.ones(n, device=dev)
+        if backface is None:
+            outs["backface"] = torch.zeros(n, dtype=torch.uint8, device=dev)
         offsets = torch.empty(P + 1, dtype=torch.int64, device=dev)
         perm = torch.empty(max(n, 1), dtype=torch.int64, device=dev) if return_perm else None
         fi, fo = _lib.Frags(), _lib.Frags()
         for f, d in ((fi, ins), (fo, outs)):
             f.width, f.height, f.npix, f.nfrag = width, height, P, n
-            for k, v in d.items():
-                setattr(f, k, ptr(v))
+            for k in ins:
+                setattr(f, k, ptr(d[k]))
         wsn = lib.woit_bin_frame_workspace_bytes(n, P)
         ws = torch.empty(max(wsn, 1), dtype=torch.uint8, device=dev)
         with torch.cuda.device(dev):

@@ -495,6 +495,46 @@ def test_bin_frame_is_the_reference_csr(W, workload, w, hgt, layers):
     assert float((a.output - b.output).abs().max()) < 1e-5
 
 
+@pytest.mark.parametrize("case", ["layer_major_core", "deep_pixel", "sparse"])
+def test_bin_frame_gather_paths(W, case):
+    """The field gather's paths: a layer-major arrival without refraction fields (core
+    fields only; the absent ones come back as the frame kernels' constants), a pixel
+    deeper than the transposed path takes (slot-by-slot copy) beside multi-chunk and
+    empty pixels, and a sparse frame (mostly empty tiles)."""
+    g = torch.Generator(device="cuda").manual_seed(11)
+    if case == "layer_major_core":
+        P, L = 3000, 37
+        pix = torch.arange(P, device="cuda", dtype=torch.int32).repeat(L)  # layer by layer
+    elif case == "deep_pixel":
+        P = 300
+        pix = torch.cat([torch.full((5000,), 7, device="cuda", dtype=torch.int32),
+                         torch.randint(0, P, (20000,), device="cuda", generator=g, dtype=torch.int32)])
+        pix = pix[torch.randperm(pix.numel(), device="cuda", generator=g)].contiguous()
+    else:
+        P = 100_000
+        pix = torch.randint(0, P // 50, (3000,), device="cuda", generator=g, dtype=torch.int32) * 50
+    n = pix.numel()
+    rnd = lambda *s: torch.rand(*s, device="cuda", generator=g)
+    depth, alpha, trans, rad = rnd(n), rnd(n), rnd(n, 3), rnd(n, 3)
+    refr = case != "layer_major_core"
+    normal, ior = (rnd(n, 3), 1.0 + rnd(n)) if refr else (None, None)
+    bf = (rnd(n) > 0.5).to(torch.uint8) if refr else None
+    fb, perm = W.FrameFragments.from_unbinned(P, 1, pix, depth, alpha, trans, rad, normal, ior, bf, return_perm=True)
+    torch.cuda.synchronize()
+    p_np = pix.cpu().numpy()
+    want = np.argsort(p_np, kind="stable")
+    np.testing.assert_array_equal(perm.cpu().numpy(), want)
+    np.testing.assert_array_equal(fb.offsets.cpu().numpy(), np.concatenate([[0], np.cumsum(np.bincount(p_np, minlength=P))]))
+    src = dict(depth=depth, alpha=alpha, trans=trans, radiance=rad)
+    if refr:
+        src.update(normal=normal, ior=ior, backface=bf)
+    for name, t in src.items():
+        np.testing.assert_array_equal(getattr(fb, name).cpu().numpy(), t.cpu().numpy()[want], name)
+    if not refr:
+        assert bool((fb.normal == torch.tensor([0.0, 0.0, -1.0], device="cuda")).all())
+        assert bool((fb.ior == 1.0).all()) and bool((fb.backface == 0).all())
+
+
 @pytest.mark.parametrize("P,n", [(1, 1000), (256, 3), (257, 100000), (70000, 1 << 20), (2_073_600, 3_000_000)])
 def test_binning_sizes(W, P, n):
     """Key widths of 0-21 bits (1-3 radix passes), tiny and ragged tiles, empty pixels."""

@@ -281,12 +281,32 @@ __global__ void __launch_bounds__(kThreads, WOIT_BIN_MINB) scatter_kernel(const 
 }
 
 // offsets[p] = lower_bound(sorted keys, p): at every key change (and the ends) the
-// thread writes the boundaries of the pixels in between (empty pixels included)
+// thread writes the boundaries of the pixels in between (empty pixels included).
+// Four keys per thread (one 16-B load; `keys` is 16-B aligned) plus the one before.
 __global__ void offsets_kernel(const int32_t* __restrict__ keys, int64_t n, int64_t npix, int64_t* __restrict__ offsets) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t lo = i == 0 ? 0 : (int64_t)keys[i - 1] + 1;  // pixels whose run starts at i
-        const int64_t hi = i == n ? npix : (int64_t)keys[i];
-        for (int64_t p = lo; p <= hi; ++p) offsets[p] = i;
+    const int64_t n4 = n / 4;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= n4; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i0 = 4 * j;
+        int k[4];
+        int cnt = 4;
+        if (j < n4) {
+            const int4 v = __ldg(reinterpret_cast<const int4*>(keys) + j);
+            k[0] = v.x, k[1] = v.y, k[2] = v.z, k[3] = v.w;
+        } else {  // the tail (< 4 keys) and the end i == n
+            cnt = (int)(n - i0);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) k[m] = m < cnt ? keys[i0 + m] : 0;
+        }
+        int64_t prev = i0 == 0 ? -1 : (int64_t)keys[i0 - 1];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            if (m < cnt) {
+                for (int64_t p = prev + 1; p <= k[m]; ++p) offsets[p] = i0 + m;  // pixels whose run starts here
+                prev = k[m];
+            }
+        }
+        if (j == n4)  // the last thread: the pixels after the last key end at n
+            for (int64_t p = prev + 1; p <= npix; ++p) offsets[p] = n;
     }
 }
 
@@ -308,8 +328,9 @@ __global__ void __launch_bounds__(kGT) gather_kernel(const int64_t* __restrict__
     extern __shared__ float gst[];  // [planes][kGK][kGP + 1] (+ backface bytes)
     constexpr int NPL = REFR ? 12 : 8;  // depth, alpha, trans 3, radiance 3 (+ normal 3, ior)
     uint8_t* gbf = reinterpret_cast<uint8_t*>(gst + NPL * kGPlane);
-    __shared__ int s_len[kGP + 1];      // chunk run-length prefix over the tile's pixels
+    __shared__ int s_len[kGP];          // chunk run-length prefix over the tile's pixels
     __shared__ int64_t s_slot[kGP];     // first slot of the pixel's chunk run
+    __shared__ uint8_t s_own[kGP * kGK];  // chunk output position -> pixel
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const bool has_a = in.alpha, has_t = in.trans, has_r = in.radiance;
     const bool has_n = REFR && in.normal, has_i = REFR && in.ior, has_b = REFR && in.backface;
@@ -370,56 +391,46 @@ __global__ void __launch_bounds__(kGT) gather_kernel(const int64_t* __restrict__
                 if (REFR) f[j][NPL - 1] = has_i ? __ldg(in.ior + x) : 0.0f;
                 fb[j] = has_b ? __ldg(in.backface + x) : 0;
             }
-            // the chunk's run per pixel, its prefix over the tile, its first slot
+            // the chunk's run per pixel and its prefix over the tile (every warp forms it)
             const int len = c_p - kc < 0 ? 0 : (c_p - kc < kGK ? c_p - kc : kGK);
-            if (w == 0) {
-                int x = len;
+            int incl = len;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, x, o);
-                    if (lane >= o) x += y;
-                }
-                s_len[lane + 1] = x;
-                if (lane == 0) s_len[0] = 0;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int excl = incl - len;
+            if (w == 0) {
+                s_len[lane] = excl;
                 s_slot[lane] = o_p + kc;
             }
 #pragma unroll
             for (int j = 0; j < KPW; ++j) {
                 if (a[j] < 0) continue;
-                const int r = (w + kGW * j) * (kGP + 1) + lane;
+                const int kk = w + kGW * j;
+                const int r = kk * (kGP + 1) + lane;
 #pragma unroll
                 for (int q = 0; q < NPL; ++q) gst[q * kGPlane + r] = f[j][q];
                 if (has_b) gbf[r] = fb[j];
+                s_own[excl + kk] = (uint8_t)lane;  // output position -> its pixel
             }
             __syncthreads();
             // write: the runs, consecutive threads on consecutive slots
-            const int tot = s_len[kGP];
-            auto locate = [&](int i, int& q, int& kk) {  // i-th slot of the chunk -> (pixel, k)
-                q = 0;
-#pragma unroll
-                for (int st = kGP / 2; st >= 1; st >>= 1)
-                    if (s_len[q + st] <= i) q += st;
-                kk = i - s_len[q];
-            };
-            for (int i = threadIdx.x; i < tot; i += kGT) {
-                int q, kk;
-                locate(i, q, kk);
+            const int tot = __shfl_sync(0xffffffffu, incl, 31);
+            for (int e = threadIdx.x; e < tot; e += kGT) {
+                const int q = s_own[e], kk = e - s_len[q];
                 const int64_t s = s_slot[q] + kk;
                 const int r = kk * (kGP + 1) + q;
                 od[s] = gst[r];
                 if (has_a) oa[s] = gst[kGPlane + r];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    if (has_t) ot[3 * s + c] = gst[(2 + c) * kGPlane + r];
+                    if (has_r) orad[3 * s + c] = gst[(5 + c) * kGPlane + r];
+                    if (has_n) on[3 * s + c] = gst[(8 + c) * kGPlane + r];
+                }
                 if (has_i) oi[s] = gst[(NPL - 1) * kGPlane + r];
                 if (has_b) ob_[s] = gbf[r];
-            }
-            for (int i = threadIdx.x; i < 3 * tot; i += kGT) {
-                const int e = i / 3, c = i - 3 * e;
-                int q, kk;
-                locate(e, q, kk);
-                const int64_t s = s_slot[q] + kk;
-                const int r = kk * (kGP + 1) + q;
-                if (has_t) ot[3 * s + c] = gst[(2 + c) * kGPlane + r];
-                if (has_r) orad[3 * s + c] = gst[(5 + c) * kGPlane + r];
-                if (has_n) on[3 * s + c] = gst[(8 + c) * kGPlane + r];
             }
             __syncthreads();
         }
@@ -486,7 +497,7 @@ cudaError_t run(const K* pix, int64_t n, int64_t npix, int64_t* offsets, const G
         vin = vo;
         cur ^= 1;
     }
-    const int64_t g2 = (n + 256) / 256;
+    const int64_t g2 = (n / 4 + 256) / 256;
     offsets_kernel<<<(unsigned)(g2 < 8192 ? g2 : 8192), 256, 0, st>>>(kin, n, npix, offsets);
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess || !g.in.depth) return err;

@@ -47,6 +47,12 @@
 #ifndef WOIT_FLAG_INSTANCES  // general-kernel instances specialised for fixed flag sets
 #define WOIT_FLAG_INSTANCES 1
 #endif
+#ifndef WOIT_GEN_FL_MINW  // resident warps per SM the flag-specialised general instances are compiled for
+#define WOIT_GEN_FL_MINW 12
+#endif
+#ifndef WOIT_NRM_PREFETCH  // general kernel: L2 bulk prefetch of the sub-tile's normals
+#define WOIT_NRM_PREFETCH 1
+#endif
 #ifndef WOIT_GEN_ALIASZ  // fused general kernel: z over the staged depth (as the fast path)
 #define WOIT_GEN_ALIASZ 1
 #endif
@@ -583,7 +589,7 @@ template <int R>
 constexpr int kMinWarps() { return R <= 3 ? WOIT_MINB : R == 4 ? 10 : R == 5 ? 6 : 4; }
 
 template <int R, bool GEN, bool FUS, int VAR, int FL>
-__global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) / WT<R>::WPB) frame_kernel(const __grid_constant__ KParams kp) {
+__global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? (FL != 0 ? WOIT_GEN_FL_MINW : 12) : kMinWarps<R>()) / WT<R>::WPB) frame_kernel(const __grid_constant__ KParams kp) {
     using G = WT<R>;
     constexpr int S = G::S, V = G::V, CH = G::CH, WC = 32, FBW = G::FBW, WIN = G::WIN, SUBP = G::SUBP;
     constexpr int AR = WC + 1;  // chunk-accumulator row stride: the (pixel, channel) combine lanes hit distinct banks
@@ -926,6 +932,10 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
                     if (do_eval) bulk_g2s(sm.rad, kp.f.radiance + 3 * a4, 12u * n4, sm.bar);
                     if (w_ior) bulk_g2s(sm.ior, kp.f.ior + a4, 4u * n4, sm.bar);
                     if (w_nrm) bulk_g2s(sm.normal, kp.f.normal + 3 * a4, 12u * n4, sm.bar);
+                    // refraction normals are read from global memory by the evaluation:
+                    // on their way into L2 while the sub-tile is built
+                    if (GEN && refr && WOIT_NRM_GLOBAL && WOIT_NRM_PREFETCH && kp.f.normal)
+                        bulk_prefetch_l2(kp.f.normal + 3 * a4, 12u * n4);
                 }
                 if (w_bf && b16 > a16) bulk_g2s(sm.bf, kp.f.backface + a16, (uint32_t)(b16 - a16), sm.bar);
             }
@@ -1110,15 +1120,29 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? 12 : kMinWarps<R>()) /
                     kp.b.refraction_offset[p * 2] = GEN ? (float)ro0 : 0.0f;
                     kp.b.refraction_offset[p * 2 + 1] = GEN ? (float)ro1 : 0.0f;
                 }
+                double acc[3], wgt[3];
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) {
-                    const double acc = 0.0 + (double)ac[ch], wgt = 0.0 + (double)wg[ch];
-                    if (kp.b.accum) kp.b.accum[p * 3 + ch] = (float)acc;
-                    if (kp.b.weight) kp.b.weight[p * 3 + ch] = (float)wgt;
-                    if (kp.b.output)
-                        kp.b.output[p * 3 + ch] =
-                            GEN ? composite_channel(kp, flags, p, ch, acc, wgt, ro0, ro1, vt[ch], dp, kPF ? tsb + ch : nullptr)
-                                : composite_fast_ch(flags, acc, wgt, (double)kp.f.opaque_color[p * 3 + ch], vt[ch]);
+                    acc[ch] = 0.0 + (double)ac[ch];
+                    wgt[ch] = 0.0 + (double)wg[ch];
+                    if (kp.b.accum) kp.b.accum[p * 3 + ch] = (float)acc[ch];
+                    if (kp.b.weight) kp.b.weight[p * 3 + ch] = (float)wgt[ch];
+                }
+                if (kp.b.output) {
+                    if (GEN) {
+                        // all three channels at once (composite_pixel: the same operations
+                        // as composite_channel's, bit for bit), so every background gather
+                        // of the pixel is in flight together
+                        float o3[3];
+                        composite_pixel(kp, flags, p, acc, wgt, ro0, ro1, vt, dp, o3, kPF ? tsb : nullptr);
+#pragma unroll
+                        for (int ch = 0; ch < 3; ++ch) kp.b.output[p * 3 + ch] = o3[ch];
+                    } else {
+#pragma unroll
+                        for (int ch = 0; ch < 3; ++ch)
+                            kp.b.output[p * 3 + ch] =
+                                composite_fast_ch(flags, acc[ch], wgt[ch], (double)kp.f.opaque_color[p * 3 + ch], vt[ch]);
+                    }
                 }
             }
             // coefficients: Haar analysis of each channel's staircase in f64, transposed

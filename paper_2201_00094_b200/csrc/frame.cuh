@@ -297,14 +297,15 @@ WOIT_D double sample_background_ch(const float* img, int W, int H, int64_t gp, i
 // gather, a bilinear sample at the refracted position, or the pixel itself. `img` is
 // [H][W][3] addressed by the pixel id gp (global with a full image, else band-local).
 WOIT_D void sample_background(const float* img, int W, int H, int64_t gp, int flags, int taps,
-                              const TapTable& tt, double ox, double oy, double bg[3]) {
+                              const TapTable& tt, double ox, double oy, double bg[3],
+                              const float* self = nullptr) {
     if (flags & (WOIT_CHROMATIC_ABERRATION | WOIT_REFRACTION)) {
         double px, py;
         pixel_xy(gp, W, px, py);
         if (ox == 0.0 && oy == 0.0 && (!(flags & WOIT_CHROMATIC_ABERRATION) || (tt.n == taps && tt.unit))) {
             // exact bilinear weights (1, 0) at the pixel, 0/1 tap weights: the pixel itself
 #pragma unroll
-            for (int ch = 0; ch < 3; ++ch) bg[ch] = (double)img[gp * 3 + ch];
+            for (int ch = 0; ch < 3; ++ch) bg[ch] = self ? (double)self[ch] : (double)img[gp * 3 + ch];
             return;
         }
         if (flags & WOIT_CHROMATIC_ABERRATION) {
@@ -329,7 +330,7 @@ WOIT_D void sample_background(const float* img, int W, int H, int64_t gp, int fl
         }
     } else {
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) bg[ch] = (double)img[gp * 3 + ch];
+        for (int ch = 0; ch < 3; ++ch) bg[ch] = self ? (double)self[ch] : (double)img[gp * 3 + ch];
     }
 }
 
@@ -343,7 +344,7 @@ WOIT_D double diffusion_weight(const KParams& kp, double dp) {
 // (only read with WOIT_DIFFUSION).
 WOIT_D void composite_pixel(const KParams& kp, int flags, int64_t p, const double acc[3],
                             const double wgt[3], double ox, double oy, const double vtot[3],
-                            double dp, float out[3]) {
+                            double dp, float out[3], const float* self = nullptr) {
     const int W = kp.f.width;
     // flags: kp.p.flags, or a compile-time copy of them (specialised kernel instances)
     double bg[3];
@@ -354,10 +355,10 @@ WOIT_D void composite_pixel(const KParams& kp, int flags, int64_t p, const doubl
     const int64_t gp = full ? kp.f.pixel_base + p : p;
     if (gather) {
         sample_background(full ? kp.b.full_opaque_image : kp.f.opaque_color, W, H, gp, flags,
-                          kp.p.aberration_taps, kp.taps, ox, oy, bg);
+                          kp.p.aberration_taps, kp.taps, ox, oy, bg, self);
     } else {
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) bg[ch] = (double)kp.f.opaque_color[p * 3 + ch];
+        for (int ch = 0; ch < 3; ++ch) bg[ch] = self ? (double)self[ch] : (double)kp.f.opaque_color[p * 3 + ch];
     }
     if (flags & WOIT_DIFFUSION) {
         // K_resolve: lerp towards the same sample of the blurred background

@@ -444,12 +444,10 @@ template <bool REFR>
 cudaError_t launch_gather(const int64_t* offsets, const int32_t* perm, int64_t npix, const Gather& g,
                           cudaStream_t st) {
     const size_t smem = gather_smem<REFR>();
-    cudaError_t err = cudaFuncSetAttribute(gather_kernel<REFR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // the opt-in attribute and the occupancy: frame.cu's cached, thread-safe query
+    int sms = 148, per = 1;
+    cudaError_t err = launch_config(reinterpret_cast<const void*>(gather_kernel<REFR>), kGT, (int)smem, sms, per);
     if (err != cudaSuccess) return err;
-    int dev = 0, sms = 148, per = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gather_kernel<REFR>, kGT, smem);
     const int64_t ntile = (npix + kGP - 1) / kGP;
     int64_t grid = (int64_t)sms * (per > 0 ? per : 1);
     grid = grid < ntile ? grid : ntile;

@@ -37,6 +37,9 @@ cudaError_t build_atomic(const int32_t* pix, const woit_frags_t& f, int rank, in
                          const float* far, float* coeffs, void* ws, cudaStream_t st);
 cudaError_t resolve_blur(const float* image, int32_t W, int32_t H, int32_t r, float* out, void* ws,
                          cudaStream_t st);
+// kernel launch geometry (frame.cu): sets the smem opt-in attribute as needed and
+// returns the SM count and resident blocks per SM, cached per (kernel, device, bytes)
+cudaError_t launch_config(const void* fn, int threads, int bytes, int& sms, int& per_sm);
 namespace synth {
 struct Out {
     float *depth, *alpha, *trans, *rad, *normal, *ior;

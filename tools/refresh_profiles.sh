@@ -12,6 +12,8 @@ python tools/config3.py > gpurun_out/c3.log 2>&1
 python tools/scenes_bench.py > gpurun_out/scenes1080.log 2>&1
 python tools/scenes_bench.py --width 3840 --height 2160 > gpurun_out/scenes4k.log 2>&1
 python tools/build_compare.py > gpurun_out/build_compare.json 2>&1
+python tools/c3_split.py > gpurun_out/c3split.json 2>&1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/binprof.csv python tools/bin_prof.py --iters 1 > gpurun_out/binprof.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 20 --warmup 3 --no-cpu --no-e2e --no-c4 > gpurun_out/ncu_bench.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:frame_kernel -c 1 -o gpurun_out/c2full python tools/profile_frame.py --iters 1 > gpurun_out/ncu_c2.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:frame_kernel -c 1 -o gpurun_out/c3full python tools/config3.py --iters 1 --no-oracle > gpurun_out/ncu_c3.log 2>&1

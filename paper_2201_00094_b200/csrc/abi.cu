@@ -82,11 +82,15 @@ int run_frame(const woit_frags_t* f, const woit_params_t* p, woit_bufs_t* b, uin
     bool al = true;
     for (const void* q : ptrs) al = al && (q == nullptr || aligned16(q));
     kp.use_tma = al ? 1 : 0;
+    // workspace: [0] window counter, [1] window-order counters, [2] long-pixel count,
+    // [3 .. 3 + long_cap) long-pixel list, then the window order (int32 per window)
     kp.win_counter = static_cast<unsigned long long*>(ws);
-    kp.long_list = static_cast<int64_t*>(ws) + 1;
+    kp.order_cnt = reinterpret_cast<unsigned*>(static_cast<int64_t*>(ws) + 1);
+    kp.long_list = static_cast<int64_t*>(ws) + 2;
     kp.long_cap = long_cap(f->nfrag);
+    kp.win_order = reinterpret_cast<int32_t*>(static_cast<int64_t*>(ws) + 3 + kp.long_cap);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    cudaError_t err = cudaMemsetAsync(ws, 0, 2 * sizeof(int64_t), st);
+    cudaError_t err = cudaMemsetAsync(ws, 0, 3 * sizeof(int64_t), st);
     if (err != cudaSuccess) return WOIT_ECUDA;
     return cuda_status(launch_frame(kp, st));
 }
@@ -110,8 +114,8 @@ const char* woit_status_string(int status) {
 }
 
 size_t woit_frame_workspace_bytes(int64_t npix, int64_t nfrag) {
-    (void)npix;
-    return (size_t)(2 + long_cap(nfrag)) * sizeof(int64_t);  // window counter, long count, long list
+    // counters, long-pixel list, window order (run_frame)
+    return (size_t)(3 + long_cap(nfrag)) * sizeof(int64_t) + (size_t)((npix + 31) / 32) * sizeof(int32_t);
 }
 
 int woit_render_band(const woit_frags_t* frags, const woit_params_t* params, woit_bufs_t* bufs, void* ws,
@@ -181,6 +185,8 @@ int woit_step4_composite(const woit_frags_t* frags, const woit_params_t* params,
     kp.long_list = nullptr;
     kp.long_cap = 0;
     kp.win_counter = nullptr;
+    kp.order_cnt = nullptr;
+    kp.win_order = nullptr;
     return cuda_status(launch_composite(kp, static_cast<cudaStream_t>(stream)));
 }
 

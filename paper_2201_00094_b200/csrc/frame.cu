@@ -53,6 +53,9 @@
 #ifndef WOIT_NRM_PREFETCH  // general kernel: L2 bulk prefetch of the sub-tile's normals
 #define WOIT_NRM_PREFETCH 1
 #endif
+#ifndef WOIT_GEN_ORDER  // fused general kernel: windows with fragments claimed first
+#define WOIT_GEN_ORDER 1
+#endif
 #ifndef WOIT_GEN_ALIASZ  // fused general kernel: z over the staged depth (as the fast path)
 #define WOIT_GEN_ALIASZ 1
 #endif
@@ -616,14 +619,19 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? (FL != 0 ? WOIT_GEN_FL
     // registers while the current one is processed.
     const int64_t nwin = (kp.f.npix + WIN - 1) / WIN;
     const int64_t nwarps = (int64_t)gridDim.x * G::WPB;
+    // Fused general kernel: windows are claimed in the order of kp.win_order (those
+    // with fragments first, window_order_kernel), so the frame ends on empty windows
+    // instead of its heaviest ones
+    const int32_t* worder = (GEN && FUS && WOIT_GEN_ORDER) ? kp.win_order : nullptr;
+    auto wmap = [&](int64_t t) -> int64_t { return (worder && t < nwin) ? (int64_t)worder[t] : t; };
     int64_t win = (int64_t)blockIdx.x * G::WPB + (threadIdx.x >> 5);
     if (win >= nwin) return;  // warp-uniform
+    win = wmap(win);
     // The claims are pipelined one window deep: the atomic for the window after next
     // is issued while the next window's id (claimed one window earlier) is consumed,
     // so its round trip is hidden behind a window of work. (Deeper -- two claims in
-    // flight, or runs of 2-8 windows per claim -- measured slower on config 3: the
-    // frame ends on its heaviest windows, and every window held ahead lengthens that
-    // tail.)
+    // flight, or runs of 2-8 windows per claim, also after the ordering below --
+    // measured slower on config 3.)
     // (Fast kernel only: in the general kernel it measured slower -- the extra live
     // register spills in the generic instance, costs occupancy in the specialised ones.)
 #if WOIT_DYN
@@ -637,11 +645,11 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? (FL != 0 ? WOIT_GEN_FL
         if (!kPipeClaims) {
             unsigned long long c = 0;
             if (lane == 0) c = atomicAdd(kp.win_counter, 1ull);
-            return nwarps + (int64_t)__shfl_sync(0xffffffffu, c, 0);
+            return wmap(nwarps + (int64_t)__shfl_sync(0xffffffffu, c, 0));
         }
         const int64_t c = nwarps + (int64_t)__shfl_sync(0xffffffffu, claim_raw, 0);
         if (lane == 0) claim_raw = atomicAdd(kp.win_counter, 1ull);
-        return c;
+        return wmap(c);
 #else
         return win + nwarps;
 #endif
@@ -1987,6 +1995,50 @@ cudaError_t launch_tiles(const KParams& kp, cudaStream_t st) {
     return err;
 }
 
+// Claim order of the fused general kernel's windows: the windows holding fragments
+// first, the empty ones after them (in any order: the results do not depend on which
+// warp takes a window, or when). One thread per window, warp-aggregated counters.
+__global__ void window_order_kernel(const int64_t* __restrict__ offsets, int64_t npix, int64_t nwin,
+                                    int32_t* __restrict__ order, unsigned* __restrict__ cnt) {
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const bool in = w < nwin;
+    bool full = false;
+    if (in) {
+        const int64_t a = w * 32, b = a + 32 < npix ? a + 32 : npix;
+        full = offsets[b] > offsets[a];
+    }
+    const unsigned mf = __ballot_sync(0xffffffffu, in && full), me = __ballot_sync(0xffffffffu, in && !full);
+    unsigned bf = 0, be = 0;
+    if (lane == 0) {
+        if (mf) bf = atomicAdd(cnt, (unsigned)__popc(mf));
+        if (me) be = atomicAdd(cnt + 1, (unsigned)__popc(me));
+    }
+    bf = __shfl_sync(0xffffffffu, bf, 0);
+    be = __shfl_sync(0xffffffffu, be, 0);
+    const unsigned lt = (1u << lane) - 1u;
+    if (in) {
+        if (full)
+            order[bf + __popc(mf & lt)] = (int32_t)w;
+        else
+            order[nwin - 1 - (int64_t)(be + __popc(me & lt))] = (int32_t)w;
+    }
+}
+
+// Sparse frames only (fewer fragments than pixels, so most windows are empty): in
+// denser frames the claim's extra dependent load outweighs the shorter tail
+// (glass-stack, 3.8 fragments per pixel: +6%).
+cudaError_t launch_window_order(KParams& kp, cudaStream_t st) {
+    if (!WOIT_GEN_ORDER || !kp.win_order || kp.f.nfrag >= kp.f.npix) {
+        kp.win_order = nullptr;
+        return cudaSuccess;
+    }
+    const int64_t nwin = (kp.f.npix + 31) / 32;
+    window_order_kernel<<<(unsigned)((nwin + 255) / 256), 256, 0, st>>>(kp.f.offsets, kp.f.npix, nwin, kp.win_order,
+                                                                         kp.order_cnt);
+    return cudaGetLastError();
+}
+
 // The fused general kernel, with instances specialised (at rank 3) for the flag
 // sets of the measured configurations: the flags fold to constants, so the code of
 // the other features drops out (a smaller kernel: fewer instruction-cache misses,
@@ -1995,8 +2047,11 @@ constexpr int kFlC3 = WOIT_REFRACTION | WOIT_CHROMATIC_ABERRATION | WOIT_CUBE_TR
 constexpr int kFlC3D = kFlC3 | WOIT_DIFFUSION;                                              // + diffusion
 constexpr int kFlRefr = WOIT_REFRACTION;                                                    // glass stacks
 template <int R>
-cudaError_t launch_general(const KParams& kp, cudaStream_t st) {
+cudaError_t launch_general(const KParams& kp_in, cudaStream_t st) {
     constexpr int TV = WOIT_THIN ? kVarThin : kVarPlain;
+    KParams kp = kp_in;
+    const cudaError_t oerr = launch_window_order(kp, st);
+    if (oerr != cudaSuccess) return oerr;
     if constexpr (R == 3 && WOIT_FLAG_INSTANCES) {
         const int fl = kp.p.flags & ~WOIT_NORMALIZE;
         if (fl == kFlC3) return launch_tiles<R, true, true, TV, kFlC3>(kp, st);

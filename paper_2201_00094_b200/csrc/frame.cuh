@@ -46,6 +46,8 @@ struct KParams {
     int64_t* long_list;  // [0] = count, [1..] = band-local pixel ids
     int64_t long_cap;
     unsigned long long* win_counter;  // dynamic window claims (zeroed per launch)
+    unsigned* order_cnt;              // [2] window-order fill counters (zeroed per launch)
+    int32_t* win_order;               // [nwin] claim order of the windows (fused general kernel)
     TapTable taps;
 };
 

@@ -30,8 +30,11 @@
 namespace woit {
 namespace bin {
 
-constexpr int kThreads = 256, kWarps = kThreads / 32, kPerThread = 16;
-constexpr int kTile = kThreads * kPerThread;  // 4096 ids per tile
+#ifndef WOIT_BIN_PER_THREAD  // ids per thread of a radix tile
+#define WOIT_BIN_PER_THREAD 16  // 4,096-id tiles (8 with 6 CTAs per SM: faster scatters, slower histograms and scans, the same total)
+#endif
+constexpr int kThreads = 256, kWarps = kThreads / 32, kPerThread = WOIT_BIN_PER_THREAD;
+constexpr int kTile = kThreads * kPerThread;  // ids per tile
 constexpr int kRadix = 256;
 
 int key_bits(int64_t npix) {
@@ -166,7 +169,7 @@ struct Gather {
 template <typename K, bool FIRST, bool LAST>
 __global__ void __launch_bounds__(kThreads, WOIT_BIN_MINB) scatter_kernel(const K* __restrict__ keys_in,
                                                               const int32_t* __restrict__ vals_in, int64_t n,
-                                                              int shift, int64_t tiles,
+                                                              int shift, int dbits, int64_t tiles,
                                                               const int32_t* __restrict__ counts,
                                                               const int32_t* __restrict__ totals,
                                                               int32_t* __restrict__ keys_out,
@@ -221,9 +224,11 @@ __global__ void __launch_bounds__(kThreads, WOIT_BIN_MINB) scatter_kernel(const 
         grp = act ? grp : ~grp;
 #pragma unroll
         for (int b = 0; b < 8; ++b) {
-            const bool bit = (d >> b) & 1;
-            const unsigned m = __ballot_sync(0xffffffffu, bit);
-            grp &= bit ? m : ~m;
+            if (b < dbits) {  // the digit's significant bits only (the top pass has fewer)
+                const bool bit = (d >> b) & 1;
+                const unsigned m = __ballot_sync(0xffffffffu, bit);
+                grp &= bit ? m : ~m;
+            }
         }
         const int before = __popc(grp & ((1u << lane) - 1u));
         // the group's leader advances the warp's running count of the digit (shared
@@ -466,6 +471,7 @@ cudaError_t run(const K* pix, int64_t n, int64_t npix, int64_t* offsets, const G
     int cur = 0;
     for (int pass = 0; pass < p.passes; ++pass) {
         const int shift = 8 * pass;
+        const int kb = key_bits(npix), dbits = kb - shift < 8 ? kb - shift : 8;
         const bool first = pass == 0, last = pass == p.passes - 1;
         if (first)
             histogram_kernel<K><<<tiles, kThreads, 0, st>>>(pix, n, shift, p.tiles, p.counts);
@@ -478,16 +484,16 @@ cudaError_t run(const K* pix, int64_t n, int64_t npix, int64_t* offsets, const G
         int32_t* vlast = g.in.depth ? vo : nullptr;
         const dim3 gr(tiles), bl(kThreads);
         if (first && last)
-            scatter_kernel<K, true, true><<<gr, bl, 0, st>>>(pix, nullptr, n, shift, p.tiles, p.counts, p.totals, ko,
+            scatter_kernel<K, true, true><<<gr, bl, 0, st>>>(pix, nullptr, n, shift, dbits, p.tiles, p.counts, p.totals, ko,
                                                              vlast, g);
         else if (first)
-            scatter_kernel<K, true, false><<<gr, bl, 0, st>>>(pix, nullptr, n, shift, p.tiles, p.counts, p.totals, ko,
+            scatter_kernel<K, true, false><<<gr, bl, 0, st>>>(pix, nullptr, n, shift, dbits, p.tiles, p.counts, p.totals, ko,
                                                               vo, g);
         else if (last)
-            scatter_kernel<int32_t, false, true><<<gr, bl, 0, st>>>(kin, vin, n, shift, p.tiles, p.counts, p.totals,
+            scatter_kernel<int32_t, false, true><<<gr, bl, 0, st>>>(kin, vin, n, shift, dbits, p.tiles, p.counts, p.totals,
                                                                     ko, vlast, g);
         else
-            scatter_kernel<int32_t, false, false><<<gr, bl, 0, st>>>(kin, vin, n, shift, p.tiles, p.counts, p.totals,
+            scatter_kernel<int32_t, false, false><<<gr, bl, 0, st>>>(kin, vin, n, shift, dbits, p.tiles, p.counts, p.totals,
                                                                      ko, vo, g);
         cudaError_t err = cudaGetLastError();
         if (err != cudaSuccess) return err;

@@ -356,6 +356,44 @@ def test_empty_frame(W):
     assert torch.all(torch.isinf(bufs.near)) and torch.all(bufs.near > 0)
 
 
+@pytest.mark.parametrize("case", ["sparse", "sparse_long", "all_empty"])
+def test_general_kernel_sparse_frames(W, case):
+    """Sparse frames in the general kernel (refraction + aberration + cubed transmission):
+    fewer fragments than pixels, so its windows are claimed heaviest-first (the
+    window-order pre-pass); with a pixel deeper than a sub-tile (long-pixel kernel) and
+    with no fragments at all. Against the oracle on the same fp32 inputs."""
+    rng = np.random.default_rng({"sparse": 1, "sparse_long": 2, "all_empty": 3}[case])
+    wd, ht = 96, 40
+    P = wd * ht
+    runs = np.zeros(P, np.int64)
+    if case != "all_empty":
+        hit = rng.choice(P, P // 12, replace=False)
+        runs[hit] = rng.integers(1, 9, hit.size)
+        if case == "sparse_long":
+            runs[rng.integers(0, P)] = 700
+    offsets = np.concatenate([[0], np.cumsum(runs)])
+    n = int(offsets[-1])
+    f = lambda *s: rng.uniform(0, 1, s).astype(np.float32)
+    depth = rng.uniform(0.5, 3.0, n).astype(np.float32)
+    nrm = rng.normal(size=(n, 3))
+    nrm[:, 2] = -np.abs(nrm[:, 2]) - 0.5
+    nrm = (nrm / np.linalg.norm(nrm, axis=1, keepdims=True)).astype(np.float32)
+    ior = np.where(rng.uniform(0, 1, n) < 0.7, 1.5, 1.0).astype(np.float32)
+    bf = (rng.uniform(0, 1, n) < 0.5).astype(np.uint8)
+    od = np.where(rng.uniform(0, 1, P) < 0.8, 4.0, np.inf).astype(np.float32)
+    oc = f(P, 3)
+    args = (wd, ht, offsets, depth, (f(n) * 0.6).astype(np.float32), f(n, 3), f(n, 3), nrm, ior, bf, od, oc)
+    flags = dict(refraction=True, chromatic_aberration=True, cube_transmission=True)
+    frame = W.FrameFragments.from_numpy(*args)
+    cfg = W.RenderConfig(rank=3, width=wd, height=ht, **flags)
+    rays = W.camera_rays(W.Camera(), wd, ht)
+    bufs = W.render_band(frame, cfg, rays, full_opaque_image=frame.opaque_color.reshape(ht, wd, 3), vhat=True)
+    torch.cuda.synchronize()
+    ref = O.render_frame(O.OFrame.from_arrays(*args), O.OConfig(rank=3, width=wd, height=ht, **flags), O.OCamera())
+    assert_close_to(bufs, ref, case)
+    np.testing.assert_allclose(h(bufs.refraction_offset), ref.refraction_offset, atol=1e-3)
+
+
 @pytest.mark.parametrize("run", [2049, 5000, 20000])
 def test_long_pixel_path(W, run):
     """Pixels deeper than one sub-tile go through the long-pixel kernel."""

@@ -1,6 +1,7 @@
 """CLI / PPM / scene files (the reference's test_cli.py:79-167)."""
 
 import os
+import sys
 
 import numpy as np
 import pytest
@@ -109,3 +110,105 @@ def test_compare_table(tmp_path):
     table = {r[0]: r[1:] for r in rows[1:]}
     assert float(table["abuffer"][0]) == 0.0 and table["abuffer"][1] == "inf"
     assert float(table["wavelet"][0]) < float(table["wboit"][0])
+    # curve columns along the centre ray: the A-buffer curve is the truth itself
+    assert [float(x) for x in table["abuffer"][2:]] == [0.0, 0.0, 0.0]
+    assert all(float(x) >= 0.0 for r in table.values() for x in r[2:])
+
+
+# ---------------------------------------------------------------------------
+# graph (the reference's test_cli.py TestGraph, cli.py:116-131, curves.py:66-111)
+
+TINY_SCENE = """
+camera pos=0,0,0 forward=0,0,1 fov=60
+plane d=1.0 alpha=0.25 transmission=0,0,0 radiance=0,0,0
+opaque_backdrop d=2.0 color=0.85,0.45,0.12
+"""
+
+
+def _rows(path):
+    return [ln.split(",") for ln in path.read_text().strip().splitlines()]
+
+
+@gpu
+def test_graph_single_plane_steps(tmp_path):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    out = tmp_path / "curve.csv"
+    assert main(["graph", "--scene", "single-plane", "--methods", "wavelet", "--rank", "3", "--samples", "64",
+                 "--out", str(out)]) == 0
+    rows = _rows(out)
+    assert rows[0] == ["z", "truth", "wavelet"]
+    body = [tuple(map(float, r)) for r in rows[1:]]
+    assert len(body) == 64
+    for z, t, w in body:
+        expect = 1.0 if z < 0.5 else 0.75
+        assert t == pytest.approx(expect, abs=1e-6)
+        if abs(z - 0.5) > 1.5 / 16:  # the interpolation ramp at the step
+            assert w == pytest.approx(expect, abs=1e-3)
+    assert all(len(c.split(".")[1]) == 6 for c in rows[1])  # fixed 6-decimal cells
+
+
+@gpu
+def test_graph_car_fog_truth_shape(tmp_path):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    out = tmp_path / "curve.csv"
+    assert main(["graph", "--scene", "car-fog", "--methods", "wavelet,mlab4", "--samples", "256",
+                 "--out", str(out)]) == 0
+    truth = np.array([float(r[1]) for r in _rows(out)[1:]])
+    assert truth[0] > 0.97 and truth[-1] < 0.2
+    drops = np.diff(truth)
+    assert drops.min() < -0.1 and np.all(drops <= 1e-9)  # a glass step; never increasing
+
+
+@gpu
+def test_graph_empty_pixel_is_one(tmp_path):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    f = tmp_path / "tiny.scene"
+    f.write_text(TINY_SCENE.replace("plane d=1.0", "plane extent=0.01,0.01 d=1.0"), encoding="utf-8")
+    out = tmp_path / "curve.csv"
+    assert main(["graph", "--scene", str(f), "--pixel", "0,0", "--samples", "32", "--out", str(out)]) == 0
+    rows = _rows(out)[1:]
+    assert len(rows) == 32 and all(float(r[1]) == 1.0 and float(r[2]) == 1.0 for r in rows)
+
+
+def test_graph_usage_errors(tmp_path, capsys):
+    assert main(["graph", "--scene", "nope", "--out", str(tmp_path / "x.csv")]) == 2
+    assert "valid presets" in capsys.readouterr().err
+    assert main(["graph", "--scene", "single-plane", "--methods", "magic", "--out", str(tmp_path / "x.csv")]) == 2
+
+
+@gpu
+@pytest.mark.parametrize("preset,pixel", [("glass-stack", (32, 32)), ("smoke-fire", (30, 34)),
+                                          ("wine-bottle", (32, 32)), ("car-fog", (40, 30))])
+def test_curves_match_reference(preset, pixel):
+    """Every curve method against the reference's own curves.extract_curves on the same
+    pixel (baseline/_ref, when installed): the reference casts with its scalar
+    cast_fragments, this repo with the device cast_frame (one fp32 rounding apart)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if not os.path.isfile(os.path.join(ref, "woit", "curves.py")):
+        pytest.skip("reference not installed (bash tools/install_ref.sh)")
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    ref_mod = pytest.importorskip("woit.curves")
+    from woit.scene import cast_fragments as ref_cast
+    from woit.scene import preset as ref_preset
+
+    from paper_2201_00094_b200.curves import CURVE_METHODS, extract_curves, pixel_stream
+
+    methods = list(CURVE_METHODS)
+    fs, _, _ = ref_cast(ref_preset(preset), pixel[0], pixel[1], 65, 65)
+    want = ref_mod.extract_curves(fs, methods, 3, 256)
+    got = extract_curves(pixel_stream(S.cast_frame(S.preset(preset), 65, 65), *pixel), methods, 3, 256)
+    np.testing.assert_allclose(got.z, want.z, atol=0)
+    np.testing.assert_allclose(got.x, want.x, atol=1e-5)
+    # the truth is a step function of x: a depth within one fp32 rounding of a sample can
+    # flip one step, so compare away from the fragment depths
+    far = np.min(np.abs(got.x[:, None] - np.array([f.depth for f in fs])[None, :]), axis=1) > 1e-5 \
+        if len(fs) else np.ones(got.x.size, bool)
+    np.testing.assert_allclose(got.truth[far], want.truth[far], atol=1e-5)
+    for m in methods:
+        np.testing.assert_allclose(got.methods[m][far], want.methods[m][far], atol=1e-4, err_msg=m)

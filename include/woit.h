@@ -20,8 +20,9 @@
  *    and the fragment's position in its run, so any row-band split yields
  *    bit-identical outputs as long as every band carries its pixel_base;
  *  - a workspace `ws` carries per-launch state (the frame kernels' window-claim
- *    counter and long-pixel list, zeroed by each call): launches that may run
- *    concurrently (different streams or host threads) must not share one.
+ *    counter, window claim order and long-pixel list, reset by each call):
+ *    launches that may run concurrently (different streams or host threads) must
+ *    not share one.
  *
  * Data layout (SoA, CSR by pixel — the reference's FrameFragments contract,
  * scene.py:367-392, in fp32 instead of f64):
@@ -135,7 +136,8 @@ const char* woit_status_string(int status);
 
 /* ---- frame path (pipeline.py) -------------------------------------------- */
 
-/* Scratch for the frame and step entry points. */
+/* Scratch for the frame and step entry points: counters, the long-pixel list and
+ * the claim order of the 32-pixel windows (sparse frames in the general kernel). */
 size_t woit_frame_workspace_bytes(int64_t npix, int64_t nfrag);
 
 /* All four passes fused over one row band, fragments read from HBM once.

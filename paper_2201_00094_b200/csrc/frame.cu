@@ -56,6 +56,9 @@
 #ifndef WOIT_GEN_ORDER  // fused general kernel: windows with fragments claimed first
 #define WOIT_GEN_ORDER 1
 #endif
+#ifndef WOIT_TAIL_SPLIT  // fast kernel: windows per warp claimed as half windows at the frame's end
+#define WOIT_TAIL_SPLIT 2
+#endif
 #ifndef WOIT_GEN_ALIASZ  // fused general kernel: z over the staged depth (as the fast path)
 #define WOIT_GEN_ALIASZ 1
 #endif
@@ -624,8 +627,22 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? (FL != 0 ? WOIT_GEN_FL
     // instead of its heaviest ones
     const int32_t* worder = (GEN && FUS && WOIT_GEN_ORDER) ? kp.win_order : nullptr;
     auto wmap = [&](int64_t t) -> int64_t { return (worder && t < nwin) ? (int64_t)worder[t] : t; };
+    // Tail split (fast kernel): the frame's last WOIT_TAIL_SPLIT windows per warp are
+    // claimed as half windows (WIN / 2 pixels), so the warps' last units -- whose end
+    // the frame waits for -- are half as long. A unit u < u1 is window u; the rest are
+    // the half windows from pixel u1 WIN on. (Pixel results do not depend on the
+    // tiling: chunk order is keyed on the global pixel.)
+    constexpr int HALF = WIN / 2;
+    const int64_t u1 = (!GEN && WOIT_TAIL_SPLIT > 0)
+                           ? (nwin > WOIT_TAIL_SPLIT * nwarps ? nwin - WOIT_TAIL_SPLIT * nwarps : 0) : nwin;
+    const int64_t nunit = u1 + (u1 < nwin ? (kp.f.npix - u1 * WIN + HALF - 1) / HALF : 0);
+    auto ustart = [&](int64_t u) -> int64_t { return u < u1 ? u * WIN : u1 * WIN + (u - u1) * HALF; };
+    auto uend = [&](int64_t u) -> int64_t {
+        const int64_t e = ustart(u) + (u < u1 ? WIN : HALF);
+        return e < kp.f.npix ? e : kp.f.npix;
+    };
     int64_t win = (int64_t)blockIdx.x * G::WPB + (threadIdx.x >> 5);
-    if (win >= nwin) return;  // warp-uniform
+    if (win >= nunit) return;  // warp-uniform
     win = wmap(win);
     // The claims are pipelined one window deep: the atomic for the window after next
     // is issued while the next window's id (claimed one window earlier) is consumed,
@@ -692,10 +709,10 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? (FL != 0 ? WOIT_GEN_FL
         }
     };
     {
-        const int64_t end = (win * WIN + WIN) < kp.f.npix ? (win * WIN + WIN) : kp.f.npix;
-        if (win * WIN + lane < end) off_lane = kp.f.offsets[win * WIN + lane];
+        const int64_t s0 = ustart(win), end = uend(win);
+        if (s0 + lane < end) off_lane = kp.f.offsets[s0 + lane];
         off_last = kp.f.offsets[end];
-        prefetch_px(win * WIN, end);
+        prefetch_px(s0, end);
     }
     // Fast path: a sub-tile's composite (phase 7) is deferred until the next
     // sub-tile's staging copies are in flight, so it hides part of their latency.
@@ -793,11 +810,11 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? (FL != 0 ? WOIT_GEN_FL
             }
         }
     };
-    int64_t next_win = nwin;
-    for (; win < nwin; win = next_win) {
+    int64_t next_win = nunit;
+    for (; win < nunit; win = next_win) {
     flush();  // the pending composite reads this window's chunk prefix
-    const int64_t w0 = win * WIN;
-    const int nq = (int)((kp.f.npix - w0) < WIN ? (kp.f.npix - w0) : WIN);
+    const int64_t w0 = ustart(win);
+    const int nq = (int)(uend(win) - w0);
     // the window's offsets relative to its first fragment (int32: a window of WIN
     // pixels holds < 2^31 fragments, include/woit.h)
     const int64_t wbase = __shfl_sync(0xffffffffu, off_lane, 0);
@@ -809,9 +826,9 @@ __global__ void __launch_bounds__(WT<R>::WPB * 32, (GEN ? (FL != 0 ? WOIT_GEN_FL
     {   // prefetch the next window's offsets (consumed one window later)
         const int64_t nw = claim();
         next_win = nw;
-        if (nw < nwin) {
-            const int64_t nw0 = nw * WIN;
-            const int64_t nend = (nw0 + WIN) < kp.f.npix ? (nw0 + WIN) : kp.f.npix;
+        if (nw < nunit) {
+            const int64_t nw0 = ustart(nw);
+            const int64_t nend = uend(nw);
             if (nw0 + lane < nend) off_lane = kp.f.offsets[nw0 + lane];
             off_last = kp.f.offsets[nend];
             prefetch_px(nw0, nend);
